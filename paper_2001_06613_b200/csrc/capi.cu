@@ -1,0 +1,519 @@
+// capi.cu — the extern "C" boundary (include/seqreg_b200.h): argument checks,
+// per-context scratch, dispatch to the template instantiations, and the host
+// pieces that are O(k) or O(n) (Thomas factorisation of the shared tridiagonal).
+#include <cmath>
+#include <cstdarg>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/seqreg_b200.h"
+#include "launch.cuh"
+
+using namespace sr;
+
+struct sr_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int sms = 148;
+  int grid_override = 0;
+  Job* job_dev = nullptr;
+  Job* job_host = nullptr;  // pinned staging
+  Job job_last{};           // content of the last upload (skip identical re-uploads)
+  bool job_valid = false;
+  double* part = nullptr;
+  size_t part_cap = 0;  // doubles
+  double* red = nullptr;
+  size_t red_cap = 0;
+  void* zbuf = nullptr;
+  size_t zbuf_bytes = 0;
+  double* aux = nullptr;  // small device scratch (temporal factors, S partial reduce)
+  size_t aux_cap = 0;
+  int* iaux = nullptr;
+  size_t iaux_cap = 0;
+};
+
+static thread_local std::string g_err;
+
+static int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(call)                                                                       \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(SR_ERR_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_));        \
+  } while (0)
+
+static int kp_of(int k) {
+  if (k <= 8) return 8;
+  if (k <= 16) return 16;
+  if (k <= 32) return 32;
+  if (k <= 64) return 64;
+  return 128;
+}
+
+static bool is_pow2(double s) {
+  int e;
+  const double m = std::frexp(s, &e);
+  return m == 0.5;
+}
+
+static Geo make_geo(const sr_grid& gr) {
+  Geo g{};
+  g.nd = gr.ndim;
+  long long st = 1;
+  g.pow2 = 1;
+  for (int a = 0; a < 3; ++a) {
+    const bool used = a < gr.ndim;
+    g.n[a] = used ? gr.dims[a] : 1;
+    g.st[a] = st;
+    st *= g.n[a];
+    g.o[a] = used ? gr.origin[a] : 0.0;
+    g.s[a] = used ? gr.spacing[a] : 1.0;
+    g.inv[a] = 1.0 / g.s[a];
+    if (used && !is_pow2(g.s[a])) g.pow2 = 0;
+  }
+  g.N = st;
+  return g;
+}
+
+static int check_grid(const sr_grid& g) {
+  if (g.ndim < 2 || g.ndim > 3) return fail(SR_ERR_ARG, "grid must be 2- or 3-dimensional, got %d axes", g.ndim);
+  for (int a = 0; a < g.ndim; ++a) {
+    if (g.dims[a] < 2) return fail(SR_ERR_ARG, "all dims must be >= 2");
+    if (!(g.spacing[a] > 0)) return fail(SR_ERR_ARG, "all spacings must be > 0");
+  }
+  return SR_OK;
+}
+
+static int ensure(void** p, size_t* cap, size_t need_bytes) {
+  if (*cap >= need_bytes) return SR_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *cap = 0;
+  CK(cudaMalloc(p, need_bytes));
+  *cap = need_bytes;
+  return SR_OK;
+}
+
+static int ensure_d(double** p, size_t* cap_doubles, size_t need) {
+  void* v = *p;
+  size_t bytes = *cap_doubles * 8;
+  int rc = ensure(&v, &bytes, need * 8);
+  *p = (double*)v;
+  *cap_doubles = bytes / 8;
+  return rc;
+}
+
+static int check_problem(sr_ctx* ctx, const sr_problem* p) {
+  if (!ctx || !p) return fail(SR_ERR_ARG, "null context or problem");
+  int rc = check_grid(p->grid);
+  if (rc) return rc;
+  if (p->dtype != SR_F32 && p->dtype != SR_F64) return fail(SR_ERR_ARG, "dtype must be SR_F32 or SR_F64");
+  if (p->feature != SR_NCC && p->feature != SR_NGF) return fail(SR_ERR_ARG, "feature must be SR_NCC or SR_NGF");
+  if (p->param != SR_AFFINE && p->param != SR_DISPLACEMENT) return fail(SR_ERR_ARG, "param must be SR_AFFINE or SR_DISPLACEMENT");
+  if (p->k < 1) return fail(SR_ERR_ARG, "subset must be nonempty");
+  if (p->k > SR_MAX_FRAMES) return fail(SR_ERR_UNSUPPORTED, "subset of %d frames exceeds SR_MAX_FRAMES=%d", p->k, SR_MAX_FRAMES);
+  if (p->feature == SR_NGF && !(p->ngf_eps > 0)) return fail(SR_ERR_ARG, "ngf_eps must be > 0");
+  if (!p->frames_dev) return fail(SR_ERR_ARG, "frames_dev is null");
+  if (!p->frame_index) return fail(SR_ERR_ARG, "frame_index is null");
+  for (int j = 0; j < p->k; ++j)
+    if (p->frame_index[j] < 0 || p->frame_index[j] >= p->nframes)
+      return fail(SR_ERR_ARG, "frame_index[%d]=%d outside 0..%d", j, p->frame_index[j], p->nframes - 1);
+  const Geo g = make_geo(p->grid);
+  if (p->pix_lo < 0 || p->pix_hi > g.N || p->pix_lo > p->pix_hi)
+    return fail(SR_ERR_ARG, "pixel range [%lld, %lld) outside [0, %lld)", (long long)p->pix_lo, (long long)p->pix_hi, g.N);
+  if (p->param == SR_DISPLACEMENT) {
+    if (!p->y_dev) return fail(SR_ERR_ARG, "y_dev is null");
+    if (p->y_stride < 1) return fail(SR_ERR_ARG, "y_stride must be >= 1");
+  } else {
+    if (!p->affine) return fail(SR_ERR_ARG, "affine parameters are null");
+    const int na = p->grid.ndim * p->grid.ndim + p->grid.ndim;
+    for (int i = 0; i < p->k * na; ++i)
+      if (!std::isfinite(p->affine[i])) return fail(SR_ERR_ARG, "affine entries must be finite");
+  }
+  return SR_OK;
+}
+
+static Args make_args(sr_ctx* ctx, const sr_problem* p) {
+  Args a{};
+  a.g = make_geo(p->grid);
+  a.frames = p->frames_dev;
+  a.shifts = p->shifts_dev;
+  a.y = p->y_dev;
+  a.y_off = p->y_off;
+  a.y_stride = p->y_stride;
+  a.job = ctx->job_dev;
+  a.K = p->k;
+  a.pix_lo = p->pix_lo;
+  a.pix_hi = p->pix_hi;
+  a.eps = p->ngf_eps;
+  return a;
+}
+
+// Stage the per-call constants (frame indices, weights, affine rows) and upload them
+// when they differ from the last upload.  Identical constants cost nothing, which keeps
+// repeated evaluations (and CUDA-graph capture of them) free of host synchronisation.
+static int upload_job(sr_ctx* ctx, const sr_problem* p, const double* weights) {
+  Job nj = ctx->job_last;
+  for (int j = 0; j < p->k; ++j) {
+    nj.frame_index[j] = p->frame_index[j];
+    if (weights) nj.weights[j] = weights[j];
+  }
+  if (p->param == SR_AFFINE) {
+    const int d = p->grid.ndim, na = d * d + d;
+    for (int j = 0; j < p->k; ++j)
+      for (int e = 0; e < na; ++e) nj.affine[j * 12 + e] = p->affine[j * na + e];
+  }
+  if (ctx->job_valid && std::memcmp(&nj, &ctx->job_last, sizeof(Job)) == 0) return SR_OK;
+  // the previous upload may still be in flight from the pinned staging buffer
+  CK(cudaStreamSynchronize(ctx->stream));
+  *ctx->job_host = nj;
+  CK(cudaMemcpyAsync(ctx->job_dev, ctx->job_host, sizeof(Job), cudaMemcpyHostToDevice, ctx->stream));
+  ctx->job_last = nj;
+  ctx->job_valid = true;
+  return SR_OK;
+}
+
+static Launch launch_of(sr_ctx* ctx) { return Launch{ctx->stream, ctx->sms, ctx->grid_override}; }
+
+#define SR_SWITCH(dtype, nd, FN, ...)                                    \
+  ((dtype) == SR_F32 ? ((nd) == 2 ? FN##_f32_d2(__VA_ARGS__) : FN##_f32_d3(__VA_ARGS__)) \
+                     : ((nd) == 2 ? FN##_f64_d2(__VA_ARGS__) : FN##_f64_d3(__VA_ARGS__)))
+
+extern "C" {
+
+int64_t sr_raw_size(int32_t k) { return (int64_t)k * k + 3 * k + 1; }
+int64_t sr_stats_size(int32_t k) { return StatsLayout(k).total; }
+int64_t sr_stats_offset(int32_t k, int32_t field) {
+  const StatsLayout L(k);
+  switch (field) {
+    case 0: return L.C;
+    case 1: return L.sigma;
+    case 2: return L.mean;
+    case 3: return L.vmax;
+    case 4: return L.degen;
+    case 5: return L.weights;
+    case 6: return L.M;
+    case 7: return L.beta;
+    case 8: return L.shift;
+    case 9: return L.Mf;
+    default: return -1;
+  }
+}
+
+int sr_abi_version(void) { return SR_ABI_VERSION; }
+const char* sr_last_error(void) { return g_err.c_str(); }
+const char* sr_status_string(int s) {
+  switch (s) {
+    case SR_OK: return "ok";
+    case SR_ERR_ARG: return "invalid argument";
+    case SR_ERR_CUDA: return "cuda error";
+    case SR_ERR_SINGULAR: return "singular system";
+    case SR_ERR_UNSUPPORTED: return "unsupported";
+    default: return "unknown";
+  }
+}
+
+int sr_create(int32_t device, sr_ctx** out) {
+  if (!out) return fail(SR_ERR_ARG, "out is null");
+  *out = nullptr;
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(SR_ERR_ARG, "device %d outside 0..%d", device, ndev - 1);
+  CK(cudaSetDevice(device));
+  sr_ctx* c = new sr_ctx();
+  c->device = device;
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  c->sms = prop.multiProcessorCount;
+  CK(cudaMalloc(&c->job_dev, sizeof(Job)));
+  CK(cudaMallocHost(&c->job_host, sizeof(Job)));
+  std::memset(c->job_host, 0, sizeof(Job));
+  *out = c;
+  return SR_OK;
+}
+
+int sr_destroy(sr_ctx* c) {
+  if (!c) return SR_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  cudaFree(c->job_dev);
+  cudaFreeHost(c->job_host);
+  cudaFree(c->part);
+  cudaFree(c->red);
+  cudaFree(c->zbuf);
+  cudaFree(c->aux);
+  cudaFree(c->iaux);
+  delete c;
+  return SR_OK;
+}
+
+int sr_set_stream(sr_ctx* c, void* stream) {
+  if (!c) return fail(SR_ERR_ARG, "null context");
+  c->stream = (cudaStream_t)stream;
+  return SR_OK;
+}
+
+int sr_set_grid_ctas(sr_ctx* c, int32_t ctas) {
+  if (!c) return fail(SR_ERR_ARG, "null context");
+  if (ctas < 0) return fail(SR_ERR_ARG, "ctas must be >= 0");
+  c->grid_override = ctas;
+  return SR_OK;
+}
+
+int sr_frame_shifts(sr_ctx* c, int32_t dtype, const void* frames, int32_t nframes, int64_t n,
+                    void* shifts) {
+  if (!c || !frames || !shifts || nframes < 1 || n < 1) return fail(SR_ERR_ARG, "bad sr_frame_shifts arguments");
+  CK(cudaSetDevice(c->device));
+  if (dtype == SR_F32)
+    k_frame_mean<float><<<nframes, 256, 0, c->stream>>>((const float*)frames, n, (float*)shifts);
+  else
+    k_frame_mean<double><<<nframes, 256, 0, c->stream>>>((const double*)frames, n, (double*)shifts);
+  CK(cudaGetLastError());
+  return SR_OK;
+}
+
+static int corr_partial_impl(sr_ctx* c, const sr_problem* p, double* raw) {
+  const int KP = kp_of(p->k);
+  const size_t stride = (size_t)KP * KP + 3 * KP;
+  const size_t want = stride * (size_t)c->sms * 4;
+  int rc = ensure_d(&c->part, &c->part_cap, want);
+  if (rc) return rc;
+  rc = ensure_d(&c->red, &c->red_cap, stride);
+  if (rc) return rc;
+  Args a = make_args(c, p);
+  const Launch L = launch_of(c);
+  CK(SR_SWITCH(p->dtype, p->grid.ndim, pass1, p->feature, p->param, KP, L, a, c->part, c->part_cap, c->red));
+  const int n = (int)sr_raw_size(p->k);
+  k_raw_pack<<<(n + 255) / 256, 256, 0, c->stream>>>(c->red, KP, p->k, (long long)(p->pix_hi - p->pix_lo), raw);
+  CK(cudaGetLastError());
+  return SR_OK;
+}
+
+int sr_corr_partial(sr_ctx* c, const sr_problem* p, double* raw_dev) {
+  int rc = check_problem(c, p);
+  if (rc) return rc;
+  if (!raw_dev) return fail(SR_ERR_ARG, "raw_dev is null");
+  CK(cudaSetDevice(c->device));
+  rc = upload_job(c, p, nullptr);
+  if (rc) return rc;
+  return corr_partial_impl(c, p, raw_dev);
+}
+
+static int finalize_impl(sr_ctx* c, const sr_problem* p, const double* raw, double h, int64_t n_total,
+                         double* stats) {
+  if (p->dtype == SR_F32)
+    k_finalize<float><<<1, 256, 0, c->stream>>>(raw, c->job_dev, p->k, p->feature, p->grid.ndim,
+                                                (double)n_total, h, (const float*)p->shifts_dev, stats);
+  else
+    k_finalize<double><<<1, 256, 0, c->stream>>>(raw, c->job_dev, p->k, p->feature, p->grid.ndim,
+                                                 (double)n_total, h, (const double*)p->shifts_dev, stats);
+  CK(cudaGetLastError());
+  return SR_OK;
+}
+
+int sr_corr_finalize(sr_ctx* c, const sr_problem* p, const double* raw_dev, const double* weights,
+                     double cell_volume, int64_t n_total, double* stats_dev) {
+  int rc = check_problem(c, p);
+  if (rc) return rc;
+  if (!raw_dev || !stats_dev || !weights) return fail(SR_ERR_ARG, "null raw/stats/weights");
+  if (n_total < 2) return fail(SR_ERR_ARG, "feature needs at least 2 values");
+  CK(cudaSetDevice(c->device));
+  rc = upload_job(c, p, weights);
+  if (rc) return rc;
+  return finalize_impl(c, p, raw_dev, cell_volume, n_total, stats_dev);
+}
+
+static int grad_impl(sr_ctx* c, const sr_problem* p, const double* stats, void* grad, int64_t g_off,
+                     int64_t g_stride) {
+  const int KP = kp_of(p->k);
+  const int d = p->grid.ndim, na = d * d + d;
+  const Launch L = launch_of(c);
+  Args a = make_args(c, p);
+  a.stats = stats;
+  const size_t esz = p->dtype == SR_F32 ? 4 : 8;
+  // affine partial scratch: pass 2 NCC [grid][KP][na]; NGF adjoint [K][blocks][na]
+  const long long npix = p->pix_hi - p->pix_lo;
+  const size_t aff_need = std::max((size_t)c->sms * 8 * KP * na,
+                                   (size_t)p->k * (size_t)((npix + 255) / 256 + 1) * na);
+  int rc = ensure_d(&c->aux, &c->aux_cap, aff_need);
+  if (rc) return rc;
+  int nblk = 0;
+  if (p->feature == SR_NCC) {
+    a.out = grad;
+    a.o_off = g_off;
+    a.o_stride = g_stride;
+    CK(SR_SWITCH(p->dtype, d, pass2, p->feature, p->param, KP, L, a, c->aux, c->aux_cap, &nblk));
+    if (p->param == SR_AFFINE) {
+      const int warps = p->k * na;
+      k_affine_rows<<<(warps * 32 + 255) / 256, 256, 0, c->stream>>>(c->aux, nblk, KP, p->k, na, 0, (double*)grad);
+      CK(cudaGetLastError());
+    }
+    return SR_OK;
+  }
+  // NGF: z over the slab extended by one slowest-axis row on each side (the adjoint stencil)
+  const Geo g = a.g;
+  const long long row = g.st[d - 1];
+  const long long zlo = std::max<long long>(0, p->pix_lo - row);
+  const long long zhi = std::min<long long>(g.N, p->pix_hi + row);
+  const long long zs = zhi - zlo;
+  rc = ensure(&c->zbuf, &c->zbuf_bytes, (size_t)p->k * d * zs * esz);
+  if (rc) return rc;
+  Args z = a;
+  z.pix_lo = zlo;
+  z.pix_hi = zhi;
+  z.out = c->zbuf;
+  z.o_off = zlo;
+  z.o_stride = zs;
+  CK(SR_SWITCH(p->dtype, d, pass2, p->feature, p->param, KP, L, z, c->aux, c->aux_cap, &nblk));
+  a.out = grad;
+  a.o_off = g_off;
+  a.o_stride = g_stride;
+  CK(SR_SWITCH(p->dtype, d, adjoint, p->param, L, a, c->zbuf, zlo, zs, c->aux, c->aux_cap, &nblk));
+  if (p->param == SR_AFFINE) {
+    const int warps = p->k * na;
+    k_affine_rows<<<(warps * 32 + 255) / 256, 256, 0, c->stream>>>(c->aux, nblk, KP, p->k, na, 1, (double*)grad);
+    CK(cudaGetLastError());
+  }
+  return SR_OK;
+}
+
+int sr_grad(sr_ctx* c, const sr_problem* p, const double* stats_dev, void* grad_dev, int64_t g_off,
+            int64_t g_stride) {
+  int rc = check_problem(c, p);
+  if (rc) return rc;
+  if (!stats_dev || !grad_dev) return fail(SR_ERR_ARG, "null stats/grad");
+  if (p->param == SR_DISPLACEMENT && g_stride < 1) return fail(SR_ERR_ARG, "g_stride must be >= 1");
+  CK(cudaSetDevice(c->device));
+  rc = upload_job(c, p, nullptr);
+  if (rc) return rc;
+  return grad_impl(c, p, stats_dev, grad_dev, g_off, g_stride);
+}
+
+int sr_evaluate(sr_ctx* c, const sr_problem* p, const double* weights, double cell_volume,
+                double* raw_dev, double* stats_dev, void* grad_dev) {
+  int rc = check_problem(c, p);
+  if (rc) return rc;
+  if (!raw_dev || !stats_dev || !weights) return fail(SR_ERR_ARG, "null raw/stats/weights");
+  const Geo g = make_geo(p->grid);
+  if (p->pix_lo != 0 || p->pix_hi != g.N) return fail(SR_ERR_ARG, "sr_evaluate covers the whole grid");
+  CK(cudaSetDevice(c->device));
+  rc = upload_job(c, p, weights);
+  if (rc) return rc;
+  rc = corr_partial_impl(c, p, raw_dev);
+  if (rc) return rc;
+  rc = finalize_impl(c, p, raw_dev, cell_volume, g.N, stats_dev);
+  if (rc) return rc;
+  if (!grad_dev) return SR_OK;
+  return grad_impl(c, p, stats_dev, grad_dev, p->y_off, p->param == SR_DISPLACEMENT ? p->y_stride : 0);
+}
+
+int sr_curvature(sr_ctx* c, const sr_problem* p, double alpha, double h, void* grad, int64_t g_off,
+                 int64_t g_stride, double* s_out) {
+  int rc = check_problem(c, p);
+  if (rc) return rc;
+  if (p->param != SR_DISPLACEMENT) return fail(SR_ERR_ARG, "the curvature regulariser acts on displacement fields");
+  if (!grad || !s_out) return fail(SR_ERR_ARG, "null grad/s_out");
+  CK(cudaSetDevice(c->device));
+  const int d = p->grid.ndim;
+  const long long npix = p->pix_hi - p->pix_lo;
+  const size_t need = (size_t)((npix + 255) / 256 + 1) * p->k * d;
+  rc = ensure_d(&c->aux, &c->aux_cap, need);
+  if (rc) return rc;
+  Args a = make_args(c, p);
+  a.out = grad;
+  a.o_off = g_off;
+  a.o_stride = g_stride;
+  int nb = 0;
+  CK(SR_SWITCH(p->dtype, d, curvature, launch_of(c), a, alpha, h, c->aux, c->aux_cap, &nb));
+  k_reduce<<<1, 256, 0, c->stream>>>(c->aux, nb, 1, 1, 1, 1, s_out);
+  CK(cudaGetLastError());
+  return SR_OK;
+}
+
+int sr_ls_predict(sr_ctx* c, int32_t dtype, int32_t n, int64_t m, const uint8_t* mask, double beta,
+                  const void* eta, const void* ref, void* zeta) {
+  if (!c || !mask || !eta || !ref || !zeta) return fail(SR_ERR_ARG, "null argument");
+  if (!(beta > 0)) return fail(SR_ERR_ARG, "beta must be > 0");
+  if (n < 2) return fail(SR_ERR_ARG, "need at least 2 frames");
+  if (m < 1) return fail(SR_ERR_ARG, "m must be >= 1");
+  // shared tridiagonal factor, exactly thomas_solve's recurrences (temporal.py:166-191)
+  std::vector<double> fac(3 * (size_t)n);
+  double* mk = fac.data();
+  double* cp = mk + n;
+  double* piv = cp + n;
+  std::vector<double> diag(n);
+  double dmax = 0.0;
+  for (int i = 0; i < n; ++i) {
+    mk[i] = mask[i] ? 1.0 : 0.0;
+    const double lap = (i == 0 || i == n - 1) ? 1.0 : 2.0;
+    diag[i] = mk[i] + beta * lap;
+    dmax = std::max(dmax, std::fabs(diag[i]));
+  }
+  const double tol = 1e-14 * dmax, off = -beta;
+  double p0 = diag[0];
+  if (std::fabs(p0) <= tol) return fail(SR_ERR_SINGULAR, "zero pivot at row 0");
+  piv[0] = p0;
+  cp[0] = off / p0;
+  for (int i = 1; i < n; ++i) {
+    const double pv = diag[i] - off * cp[i - 1];
+    if (std::fabs(pv) <= tol) return fail(SR_ERR_SINGULAR, "zero pivot at row %d", i);
+    piv[i] = pv;
+    cp[i] = i < n - 1 ? off / pv : 0.0;
+  }
+  CK(cudaSetDevice(c->device));
+  int rc = ensure_d(&c->aux, &c->aux_cap, fac.size());
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(c->aux, fac.data(), fac.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  const int blocks = (int)((m + 255) / 256);
+  if (dtype == SR_F32)
+    k_ls_predict<float><<<blocks, 256, 0, c->stream>>>(n, m, c->aux, beta, (const float*)eta, (const float*)ref, (float*)zeta);
+  else
+    k_ls_predict<double><<<blocks, 256, 0, c->stream>>>(n, m, c->aux, beta, (const double*)eta, (const double*)ref, (double*)zeta);
+  CK(cudaGetLastError());
+  // the host factor buffer is stack/heap memory: make the copy complete before returning
+  CK(cudaStreamSynchronize(c->stream));
+  return SR_OK;
+}
+
+int sr_interp_linear(sr_ctx* c, int32_t dtype, int32_t n, int64_t m, const int32_t* left,
+                     const int32_t* right, const double* theta, const void* src, void* zeta) {
+  if (!c || !left || !right || !theta || !src || !zeta) return fail(SR_ERR_ARG, "null argument");
+  if (n < 1 || m < 1) return fail(SR_ERR_ARG, "bad sizes");
+  CK(cudaSetDevice(c->device));
+  // pack [left | right] as ints and theta as doubles into device scratch
+  void* ip = c->iaux;
+  size_t icap = c->iaux_cap * 4;
+  int rc = ensure(&ip, &icap, (size_t)2 * n * 4);
+  if (rc) return rc;
+  c->iaux = (int*)ip;
+  c->iaux_cap = icap / 4;
+  rc = ensure_d(&c->aux, &c->aux_cap, n);
+  if (rc) return rc;
+  std::vector<int> lr(2 * (size_t)n);
+  for (int i = 0; i < n; ++i) {
+    lr[i] = left[i];
+    lr[n + i] = right[i];
+  }
+  CK(cudaMemcpyAsync(c->iaux, lr.data(), lr.size() * 4, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->aux, theta, (size_t)n * 8, cudaMemcpyHostToDevice, c->stream));
+  dim3 grid((unsigned)((m + 255) / 256), n);
+  if (dtype == SR_F32)
+    k_interp_linear<float><<<grid, 256, 0, c->stream>>>(n, m, c->iaux, c->iaux + n, c->aux, (const float*)src, (float*)zeta);
+  else
+    k_interp_linear<double><<<grid, 256, 0, c->stream>>>(n, m, c->iaux, c->iaux + n, c->aux, (const double*)src, (double*)zeta);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(c->stream));
+  return SR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,5 @@
+// Explicit instantiation unit: dtype float, 3-D grids (all features, parametrisations, KP).
+#include "launch.cuh"
+namespace sr {
+SR_DEFINE_INST(f32, float, 3)
+}  // namespace sr

@@ -1,0 +1,5 @@
+// Explicit instantiation unit: dtype double, 3-D grids (all features, parametrisations, KP).
+#include "launch.cuh"
+namespace sr {
+SR_DEFINE_INST(f64, double, 3)
+}  // namespace sr

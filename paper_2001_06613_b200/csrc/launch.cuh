@@ -1,0 +1,187 @@
+// launch.cuh — host-side launchers for one (T, D, FEAT, PARAM, KP) combination.
+// Included by the per-(dtype, ndim) instantiation units inst_*.cu.
+#pragma once
+#include <cstdio>
+#include "engine.cuh"
+
+namespace sr {
+
+struct Launch {
+  cudaStream_t stream;
+  int sms;
+  int grid_override;  // 0 = auto
+};
+
+template <typename K>
+static int occupancy_grid(const Launch& L, K kernel, int nt, size_t smem, long long ntiles) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, nt, smem);
+  if (per_sm < 1) per_sm = 1;
+  long long g = (long long)per_sm * L.sms;
+  if (L.grid_override > 0) g = L.grid_override;
+  if (g > ntiles) g = ntiles;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+template <typename T, int D, int FEAT, int PARAM, int KP>
+struct Runner {
+  // pass 1 + cross-CTA reduce; returns number of CTAs used, writes red[KP*KP+2KP]
+  static cudaError_t pass1(const Launch& L, const Args& a, double* part, size_t part_cap,
+                           double* red) {
+    using C = G1<T, KP>;
+    using Tl = Tile1<T, D, FEAT, KP>;
+    const size_t smem = pass1_smem<T, D, FEAT, PARAM, KP>();
+    auto kern = k_pass1<T, D, FEAT, PARAM, KP>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const long long npix = a.pix_hi - a.pix_lo;
+    const long long ntiles = (npix + Tl::TP - 1) / Tl::TP;
+    int grid = occupancy_grid(L, kern, C::NT, smem, ntiles > 0 ? ntiles : 1);
+    const size_t stride = (size_t)KP * KP + 3 * KP;
+    if ((size_t)grid * stride > part_cap) grid = (int)(part_cap / stride);
+    Args b = a;
+    b.part = part;
+    kern<<<grid, C::NT, smem, L.stream>>>(b);
+    const int n_total = (int)stride;
+    k_reduce<<<(n_total + 31) / 32, 256, 0, L.stream>>>(part, grid, (int)stride, KP * KP + KP,
+                                                          KP * KP + 3 * KP, n_total, red);
+    return cudaGetLastError();
+  }
+
+  static cudaError_t pass2(const Launch& L, const Args& a, double* part_aff, size_t aff_cap,
+                           int* nblk_out) {
+    using C = G2<T, KP>;
+    constexpr int NA = D * (D + 1);
+    size_t smem = pass2_smem<T, D, FEAT, KP>();
+    const size_t need_red = (size_t)NA * C::NT * 8;
+    if (smem < need_red) smem = need_red;
+    auto kern = k_pass2<T, D, FEAT, PARAM, KP>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const long long npix = a.pix_hi - a.pix_lo;
+    const long long ntiles = (npix + C::TP - 1) / C::TP;
+    int grid = occupancy_grid(L, kern, C::NT, smem, ntiles > 0 ? ntiles : 1);
+    if (PARAM == AFFINE && FEAT == NCC) {
+      const size_t stride = (size_t)KP * NA;
+      if ((size_t)grid * stride > aff_cap) grid = (int)(aff_cap / stride);
+    }
+    Args b = a;
+    b.part_aff = part_aff;
+    kern<<<grid, C::NT, smem, L.stream>>>(b);
+    *nblk_out = grid;
+    return cudaGetLastError();
+  }
+};
+
+template <typename T, int D, int PARAM>
+cudaError_t run_ngf_adjoint(const Launch& L, const Args& a, const T* zb, long long z_off,
+                            long long z_stride, double* part_aff, size_t aff_cap, int* nblk_out) {
+  const long long npix = a.pix_hi - a.pix_lo;
+  const int gx = (int)((npix + 255) / 256);
+  constexpr int NA = D * (D + 1);
+  if (PARAM == AFFINE && (size_t)gx * a.K * NA > aff_cap) return cudaErrorInvalidValue;
+  dim3 grid(gx > 0 ? gx : 1, a.K);
+  Args b = a;
+  b.part_aff = part_aff;
+  k_ngf_adjoint<T, D, PARAM><<<grid, 256, 0, L.stream>>>(b, zb, z_off, z_stride);
+  *nblk_out = grid.x;
+  return cudaGetLastError();
+}
+
+template <typename T, int D>
+cudaError_t run_curvature(const Launch& L, const Args& a, double alpha, double h, double* part,
+                          size_t cap, int* nblk_out) {
+  const long long npix = a.pix_hi - a.pix_lo;
+  const int gx = (int)((npix + 255) / 256);
+  dim3 grid(gx > 0 ? gx : 1, a.K * D);
+  if ((size_t)grid.x * grid.y > cap) return cudaErrorInvalidValue;
+  k_curvature<T, D><<<grid, 256, 0, L.stream>>>(a, alpha, h, part);
+  *nblk_out = grid.x * grid.y;
+  return cudaGetLastError();
+}
+
+// Dispatch over (FEAT, PARAM, KP) for fixed (T, D).
+template <typename T, int D>
+struct Dispatch {
+  template <int FEAT, int PARAM>
+  static cudaError_t p1k(int KP, const Launch& L, const Args& a, double* part, size_t cap, double* red) {
+    switch (KP) {
+      case 8: return Runner<T, D, FEAT, PARAM, 8>::pass1(L, a, part, cap, red);
+      case 16: return Runner<T, D, FEAT, PARAM, 16>::pass1(L, a, part, cap, red);
+      case 32: return Runner<T, D, FEAT, PARAM, 32>::pass1(L, a, part, cap, red);
+      case 64: return Runner<T, D, FEAT, PARAM, 64>::pass1(L, a, part, cap, red);
+      default: return Runner<T, D, FEAT, PARAM, 128>::pass1(L, a, part, cap, red);
+    }
+  }
+  template <int FEAT, int PARAM>
+  static cudaError_t p2k(int KP, const Launch& L, const Args& a, double* pa, size_t cap, int* nb) {
+    switch (KP) {
+      case 8: return Runner<T, D, FEAT, PARAM, 8>::pass2(L, a, pa, cap, nb);
+      case 16: return Runner<T, D, FEAT, PARAM, 16>::pass2(L, a, pa, cap, nb);
+      case 32: return Runner<T, D, FEAT, PARAM, 32>::pass2(L, a, pa, cap, nb);
+      case 64: return Runner<T, D, FEAT, PARAM, 64>::pass2(L, a, pa, cap, nb);
+      default: return Runner<T, D, FEAT, PARAM, 128>::pass2(L, a, pa, cap, nb);
+    }
+  }
+  static cudaError_t pass1(int feat, int param, int KP, const Launch& L, const Args& a,
+                           double* part, size_t cap, double* red) {
+    if (feat == NCC) return param == AFFINE ? p1k<NCC, AFFINE>(KP, L, a, part, cap, red)
+                                            : p1k<NCC, DISP>(KP, L, a, part, cap, red);
+    return param == AFFINE ? p1k<NGF, AFFINE>(KP, L, a, part, cap, red)
+                           : p1k<NGF, DISP>(KP, L, a, part, cap, red);
+  }
+  static cudaError_t pass2(int feat, int param, int KP, const Launch& L, const Args& a,
+                           double* pa, size_t cap, int* nb) {
+    if (feat == NCC) return param == AFFINE ? p2k<NCC, AFFINE>(KP, L, a, pa, cap, nb)
+                                            : p2k<NCC, DISP>(KP, L, a, pa, cap, nb);
+    return param == AFFINE ? p2k<NGF, AFFINE>(KP, L, a, pa, cap, nb)
+                           : p2k<NGF, DISP>(KP, L, a, pa, cap, nb);
+  }
+  static cudaError_t adjoint(int param, const Launch& L, const Args& a, const void* zb, long long zo,
+                             long long zs, double* pa, size_t cap, int* nb) {
+    const T* z = reinterpret_cast<const T*>(zb);
+    return param == AFFINE ? run_ngf_adjoint<T, D, AFFINE>(L, a, z, zo, zs, pa, cap, nb)
+                           : run_ngf_adjoint<T, D, DISP>(L, a, z, zo, zs, pa, cap, nb);
+  }
+  static cudaError_t curvature(const Launch& L, const Args& a, double alpha, double h, double* part,
+                               size_t cap, int* nb) {
+    return run_curvature<T, D>(L, a, alpha, h, part, cap, nb);
+  }
+};
+
+// Entry points implemented in inst_<dtype>_d<D>.cu
+#define SR_DECLARE_INST(TT, DD)                                                               \
+  cudaError_t pass1_##TT##_d##DD(int feat, int param, int KP, const Launch& L, const Args& a, \
+                                 double* part, size_t cap, double* red);                     \
+  cudaError_t pass2_##TT##_d##DD(int feat, int param, int KP, const Launch& L, const Args& a, \
+                                 double* pa, size_t cap, int* nb);                           \
+  cudaError_t adjoint_##TT##_d##DD(int param, const Launch& L, const Args& a, const void* zb, \
+                                   long long zo, long long zs, double* pa, size_t cap, int* nb); \
+  cudaError_t curvature_##TT##_d##DD(const Launch& L, const Args& a, double alpha, double h,  \
+                                     double* part, size_t cap, int* nb);
+
+#define SR_DEFINE_INST(TT, T, DD)                                                             \
+  cudaError_t pass1_##TT##_d##DD(int feat, int param, int KP, const Launch& L, const Args& a, \
+                                 double* part, size_t cap, double* red) {                    \
+    return Dispatch<T, DD>::pass1(feat, param, KP, L, a, part, cap, red);                     \
+  }                                                                                           \
+  cudaError_t pass2_##TT##_d##DD(int feat, int param, int KP, const Launch& L, const Args& a, \
+                                 double* pa, size_t cap, int* nb) {                          \
+    return Dispatch<T, DD>::pass2(feat, param, KP, L, a, pa, cap, nb);                        \
+  }                                                                                           \
+  cudaError_t adjoint_##TT##_d##DD(int param, const Launch& L, const Args& a, const void* zb, \
+                                   long long zo, long long zs, double* pa, size_t cap, int* nb) { \
+    return Dispatch<T, DD>::adjoint(param, L, a, zb, zo, zs, pa, cap, nb);                    \
+  }                                                                                           \
+  cudaError_t curvature_##TT##_d##DD(const Launch& L, const Args& a, double alpha, double h,  \
+                                     double* part, size_t cap, int* nb) {                     \
+    return Dispatch<T, DD>::curvature(L, a, alpha, h, part, cap, nb);                         \
+  }
+
+SR_DECLARE_INST(f32, 2)
+SR_DECLARE_INST(f32, 3)
+SR_DECLARE_INST(f64, 2)
+SR_DECLARE_INST(f64, 3)
+
+}  // namespace sr

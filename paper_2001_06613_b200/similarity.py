@@ -1,0 +1,215 @@
+"""Drop-in replacement of the reference hot path (similarity.py:128-220) on the B200 engine.
+
+Same names, argument meaning and error behaviour as
+/root/reference/pkg/src/seqreg/similarity.py:
+
+    correlation_state(seq, stack, subset, weights, cell_volume, threads=1)   (128-164)
+    dissimilarity(state)                                                     (167-177)
+    dissimilarity_gradient(state, seq, stack, subset, threads=1)             (180-220)
+
+``threads`` is accepted and ignored (the device does the parallel work).  The
+warp, feature, Gram, centring and gradient all run in the CUDA kernels of
+``libseqreg_b200.so``; only K x K host arithmetic (``dissimilarity``) stays in
+Python, exactly as in the reference.  ``install()`` rebinds the names that
+``seqreg.temporal`` resolves at call time (temporal.py:35-41), so the
+reference's multilevel drivers run unchanged on the GPU.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from .engine import EvalPlan, get_engine
+
+__all__ = [
+    "CorrelationState",
+    "configure",
+    "correlation_state",
+    "dissimilarity",
+    "dissimilarity_gradient",
+    "decompose",
+    "min_consecutive_rho",
+    "install",
+    "uninstall",
+]
+
+_OPTIONS = {"dtype": torch.float64, "feature": "ncc", "ngf_eps": 0.1}
+
+
+def configure(*, dtype=None, feature=None, ngf_eps=None) -> dict:
+    """Set the arithmetic type (float64 = the reference's, float32) and feature (ncc/ngf)."""
+    if dtype is not None:
+        if dtype not in (torch.float32, torch.float64):
+            raise ValueError("dtype must be torch.float32 or torch.float64")
+        _OPTIONS["dtype"] = dtype
+    if feature is not None:
+        if feature not in ("ncc", "ngf"):
+            raise ValueError("feature must be 'ncc' or 'ngf'")
+        _OPTIONS["feature"] = feature
+    if ngf_eps is not None:
+        if not ngf_eps > 0:
+            raise ValueError("ngf_eps must be > 0")
+        _OPTIONS["ngf_eps"] = float(ngf_eps)
+    return dict(_OPTIONS)
+
+
+def _validate_subset(stack, subset) -> tuple:
+    """similarity.py:90-99."""
+    subset = tuple(int(k) for k in subset)
+    if not subset:
+        raise ValueError("subset must be nonempty")
+    if any(k1 <= k0 for k0, k1 in zip(subset, subset[1:])):
+        raise ValueError("subset indices must be strictly increasing")
+    missing = [k for k in subset if k not in stack.items]
+    if missing:
+        raise ValueError(f"stack has no transform for frames {missing}")
+    return subset
+
+
+def _affine_rows(stack, subset) -> np.ndarray:
+    rows = []
+    for k in subset:
+        t = stack.items[k]
+        rows.append(np.concatenate([np.asarray(t.matrix, dtype=np.float64).ravel(),
+                                    np.asarray(t.translation, dtype=np.float64).ravel()]))
+    return np.ascontiguousarray(np.array(rows))
+
+
+@dataclass
+class CorrelationState:
+    """Mirror of similarity.py:109-125.
+
+    ``corr``, ``degenerate``, ``center_norms`` and ``weights`` are host arrays
+    like the reference's.  The N x K feature matrix is never materialised: the
+    gradient pass re-warps the frames on the device instead.
+    """
+
+    subset: tuple
+    corr: np.ndarray
+    weights: np.ndarray
+    cell_volume: float
+    degenerate: np.ndarray
+    center_norms: np.ndarray
+    means: np.ndarray = field(default=None, repr=False)
+    _plan: EvalPlan = field(default=None, repr=False, compare=False)
+
+    @property
+    def features(self):
+        raise AttributeError(
+            "features are virtual on the B200 engine (never stored in HBM); "
+            "use corr / center_norms, or the reference implementation for the N x K matrix"
+        )
+
+
+def correlation_state(seq, stack, subset, weights, cell_volume: float, threads: int = 1) -> CorrelationState:
+    """Warp the subset frames, extract features, and correlate them (similarity.py:128-164)."""
+    subset = _validate_subset(stack, subset)
+    w = np.asarray(weights, dtype=np.float64)
+    if w.size != len(subset):
+        raise ValueError("one weight per subset frame required")
+    if seq.grid.ndim != stack.dim:
+        raise ValueError(f"points have dimension {seq.grid.ndim}, transform has {stack.dim}")
+    eng = get_engine()
+    frames = eng.frames_for(seq, _OPTIONS["dtype"])
+    plan = EvalPlan(frames, [k - 1 for k in subset], feature=_OPTIONS["feature"], ngf_eps=_OPTIONS["ngf_eps"])
+    prob = plan.problem(affine=_affine_rows(stack, subset))
+    plan.corr_partial(prob)
+    plan.finalize(prob, w, float(cell_volume))
+    st = plan.host_stats()
+    return CorrelationState(
+        subset=subset,
+        corr=st["corr"],
+        weights=w,
+        cell_volume=float(cell_volume),
+        degenerate=st["degenerate"],
+        center_norms=st["sigma"],
+        means=st["mean"],
+        _plan=plan,
+    )
+
+
+def dissimilarity(state) -> float:
+    """D = cell_volume * sum_{i != j} w_i w_j (1 - rho_ij^2), clamped at 0 (similarity.py:167-177)."""
+    w = state.weights
+    pair_mass = w.sum() ** 2 - (w * w).sum()
+    m = np.outer(w, w) * state.corr**2
+    coupling = m.sum() - np.trace(m)
+    return max(0.0, state.cell_volume * (pair_mass - coupling))
+
+
+def dissimilarity_gradient(state, seq, stack, subset, threads: int = 1) -> np.ndarray:
+    """Analytic gradient w.r.t. the affine parameters, rows in subset order, vec(A) ++ b
+    (similarity.py:180-220).  Degenerate frames give zero rows."""
+    subset = _validate_subset(stack, subset)
+    if subset != tuple(state.subset):
+        raise ValueError("subset does not match the correlation state")
+    plan = getattr(state, "_plan", None)
+    if plan is None:
+        raise ValueError("state was not produced by the B200 correlation_state")
+    d = stack.dim
+    prob = plan.problem(affine=_affine_rows(stack, subset))
+    out = torch.empty(len(subset) * (d * d + d), dtype=torch.float64, device=plan.frames.data.device)
+    plan.grad(prob, out)
+    return out.cpu().numpy().reshape(len(subset), d * d + d)
+
+
+def decompose(seq, stack, weights, cell_volume: float, inner_subset):
+    """Within / within / cross split of D (similarity.py:223-253) on the engine's C."""
+    all_frames = stack.indices
+    inner = tuple(sorted(int(k) for k in inner_subset))
+    if not inner or set(inner) - set(all_frames):
+        raise ValueError("inner subset must be a nonempty subset of the stack's frames")
+    if len(inner) == len(all_frames):
+        raise ValueError("inner subset must be a proper subset")
+    state = correlation_state(seq, stack, all_frames, weights, cell_volume)
+    w = state.weights
+    terms = np.outer(w, w) * (1.0 - state.corr**2)
+    np.fill_diagonal(terms, 0.0)
+    mask = np.isin(all_frames, inner)
+    d_inner = cell_volume * terms[np.ix_(mask, mask)].sum()
+    d_outer = cell_volume * terms[np.ix_(~mask, ~mask)].sum()
+    d_mixed = cell_volume * (terms[np.ix_(mask, ~mask)].sum() + terms[np.ix_(~mask, mask)].sum())
+    return float(d_inner), float(d_outer), float(d_mixed)
+
+
+def min_consecutive_rho(seq, stack) -> float:
+    """Minimum correlation between consecutive transformed frames (similarity.py:256-266)."""
+    if seq.frame_count < 2:
+        raise ValueError("need at least 2 frames")
+    n = seq.frame_count
+    state = correlation_state(seq, stack, tuple(range(1, n + 1)), np.ones(n), 1.0)
+    return float(min(state.corr[i, i + 1] for i in range(n - 1)))
+
+
+_SAVED: dict = {}
+
+
+def install(module=None):
+    """Rebind seqreg.temporal's hot-path names to the B200 engine.
+
+    temporal.py imports correlation_state / dissimilarity / dissimilarity_gradient
+    into its module globals (temporal.py:35-41) and resolves them at call time,
+    so rebinding those three names routes every objective evaluation of
+    ``_gir_solve`` and ``dissim_all_frames`` through the GPU.  ``seqreg.similarity``
+    itself is left untouched (it stays the CPU oracle)."""
+    if module is None:
+        import seqreg.temporal as module  # noqa: PLC0415
+    if id(module) not in _SAVED:
+        _SAVED[id(module)] = (module, {n: getattr(module, n) for n in
+                                       ("correlation_state", "dissimilarity", "dissimilarity_gradient")})
+    module.correlation_state = correlation_state
+    module.dissimilarity = dissimilarity
+    module.dissimilarity_gradient = dissimilarity_gradient
+    return module
+
+
+def uninstall(module=None) -> None:
+    if module is None:
+        import seqreg.temporal as module  # noqa: PLC0415
+    saved = _SAVED.pop(id(module), None)
+    if saved is not None:
+        for n, f in saved[1].items():
+            setattr(saved[0], n, f)
