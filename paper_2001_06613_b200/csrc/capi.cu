@@ -1,8 +1,10 @@
 // capi.cu — the extern "C" boundary (include/seqreg_b200.h): argument checks,
 // per-context scratch, dispatch to the template instantiations, and the host
 // pieces that are O(k) or O(n) (Thomas factorisation of the shared tridiagonal).
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -17,14 +19,15 @@ struct sr_ctx {
   cudaStream_t stream = nullptr;
   int sms = 148;
   int grid_override = 0;
+  int legacy = 0;  // SEQREG_B200_LEGACY=1: non-specialized kernels only
+  int dbg = 0;     // SEQREG_B200_DEBUG: profiling experiment bits
   Job* job_dev = nullptr;
   Job* job_host = nullptr;  // pinned staging
   Job job_last{};           // content of the last upload (skip identical re-uploads)
   bool job_valid = false;
   double* part = nullptr;
   size_t part_cap = 0;  // doubles
-  double* red = nullptr;
-  size_t red_cap = 0;
+  unsigned* ticket = nullptr;  // last-block ticket of k_reduce_finalize
   void* zbuf = nullptr;
   size_t zbuf_bytes = 0;
   double* aux = nullptr;  // small device scratch (temporal factors, S partial reduce)
@@ -79,6 +82,10 @@ static Geo make_geo(const sr_grid& gr) {
     g.o[a] = used ? gr.origin[a] : 0.0;
     g.s[a] = used ? gr.spacing[a] : 1.0;
     g.inv[a] = 1.0 / g.s[a];
+    g.sti[a] = (int)g.st[a];
+    g.of[a] = (float)g.o[a];
+    g.sf[a] = (float)g.s[a];
+    g.invf[a] = (float)g.inv[a];
     if (used && !is_pow2(g.s[a])) g.pow2 = 0;
   }
   g.N = st;
@@ -129,6 +136,7 @@ static int check_problem(sr_ctx* ctx, const sr_problem* p) {
     if (p->frame_index[j] < 0 || p->frame_index[j] >= p->nframes)
       return fail(SR_ERR_ARG, "frame_index[%d]=%d outside 0..%d", j, p->frame_index[j], p->nframes - 1);
   const Geo g = make_geo(p->grid);
+  if (g.N > 2147483647LL) return fail(SR_ERR_UNSUPPORTED, "frames of more than 2^31-1 cells are not supported");
   if (p->pix_lo < 0 || p->pix_hi > g.N || p->pix_lo > p->pix_hi)
     return fail(SR_ERR_ARG, "pixel range [%lld, %lld) outside [0, %lld)", (long long)p->pix_lo, (long long)p->pix_hi, g.N);
   if (p->param == SR_DISPLACEMENT) {
@@ -156,6 +164,7 @@ static Args make_args(sr_ctx* ctx, const sr_problem* p) {
   a.pix_lo = p->pix_lo;
   a.pix_hi = p->pix_hi;
   a.eps = p->ngf_eps;
+  a.dbg = ctx->dbg;
   return a;
 }
 
@@ -183,11 +192,68 @@ static int upload_job(sr_ctx* ctx, const sr_problem* p, const double* weights) {
   return SR_OK;
 }
 
-static Launch launch_of(sr_ctx* ctx) { return Launch{ctx->stream, ctx->sms, ctx->grid_override}; }
+static Launch launch_of(sr_ctx* ctx) {
+  return Launch{ctx->stream, ctx->sms, ctx->grid_override, ctx->legacy};
+}
 
 #define SR_SWITCH(dtype, nd, FN, ...)                                    \
   ((dtype) == SR_F32 ? ((nd) == 2 ? FN##_f32_d2(__VA_ARGS__) : FN##_f32_d3(__VA_ARGS__)) \
                      : ((nd) == 2 ? FN##_f64_d2(__VA_ARGS__) : FN##_f64_d3(__VA_ARGS__)))
+
+template <typename T>
+static cudaError_t launch_reduce_finalize(sr_ctx* c, const sr_problem* p, int nblk, int KP, long long count,
+                                          double* raw, int do_final, double h, double* stats) {
+  const size_t dsm = do_final ? (size_t)p->k * p->k * 8 : 0;
+  auto kern = k_reduce_finalize<T>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(dsm, 1));
+  if (e != cudaSuccess) return e;
+  const int stride = KP * KP + 3 * KP;
+  kern<<<(stride + 31) / 32, 1024, dsm, c->stream>>>(c->part, nblk, KP, p->k, count, raw, do_final, c->job_dev,
+                                                      p->feature, p->grid.ndim, h, (const T*)p->shifts_dev,
+                                                      stats, c->ticket);
+  return cudaGetLastError();
+}
+
+// pass 1 over the slab, then the fixed-order cross-CTA reduction into raw (and, with
+// stats != nullptr, the finalize in the same launch)
+static int corr_partial_impl(sr_ctx* c, const sr_problem* p, double* raw, double h = 0.0,
+                             double* stats = nullptr) {
+  const int KP = kp_of(p->k);
+  const size_t stride = (size_t)KP * KP + 3 * KP;
+  const size_t want = stride * (size_t)c->sms * 4;
+  int rc = ensure_d(&c->part, &c->part_cap, want);
+  if (rc) return rc;
+  Args a = make_args(c, p);
+  const Launch L = launch_of(c);
+  int nblk = 0;
+  CK(SR_SWITCH(p->dtype, p->grid.ndim, pass1, p->feature, p->param, KP, L, a, c->part, c->part_cap, &nblk));
+  const long long count = (long long)(p->pix_hi - p->pix_lo);
+  const int fin = stats != nullptr;
+  if (p->dtype == SR_F32)
+    CK(launch_reduce_finalize<float>(c, p, nblk, KP, count, raw, fin, h, stats));
+  else
+    CK(launch_reduce_finalize<double>(c, p, nblk, KP, count, raw, fin, h, stats));
+  return SR_OK;
+}
+
+template <typename T>
+static cudaError_t launch_finalize(sr_ctx* c, const sr_problem* p, const double* raw, double h, int64_t n_total,
+                                   double* stats) {
+  const size_t dsm = (size_t)p->k * p->k * 8;
+  auto kern = k_finalize<T>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
+  if (e != cudaSuccess) return e;
+  kern<<<1, 1024, dsm, c->stream>>>(raw, c->job_dev, p->k, p->feature, p->grid.ndim, (double)n_total, h,
+                                    (const T*)p->shifts_dev, stats);
+  return cudaGetLastError();
+}
+
+static int finalize_impl(sr_ctx* c, const sr_problem* p, const double* raw, double h, int64_t n_total,
+                         double* stats) {
+  if (p->dtype == SR_F32) CK(launch_finalize<float>(c, p, raw, h, n_total, stats));
+  else CK(launch_finalize<double>(c, p, raw, h, n_total, stats));
+  return SR_OK;
+}
 
 extern "C" {
 
@@ -235,7 +301,15 @@ int sr_create(int32_t device, sr_ctx** out) {
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, device));
   c->sms = prop.multiProcessorCount;
+  {
+    const char* lg = getenv("SEQREG_B200_LEGACY");
+    c->legacy = (lg && lg[0] == '1') ? 1 : 0;
+    const char* db = getenv("SEQREG_B200_DEBUG");
+    c->dbg = db ? atoi(db) : 0;
+  }
   CK(cudaMalloc(&c->job_dev, sizeof(Job)));
+  CK(cudaMalloc(&c->ticket, sizeof(unsigned)));
+  CK(cudaMemset(c->ticket, 0, sizeof(unsigned)));
   CK(cudaMallocHost(&c->job_host, sizeof(Job)));
   std::memset(c->job_host, 0, sizeof(Job));
   *out = c;
@@ -249,7 +323,7 @@ int sr_destroy(sr_ctx* c) {
   cudaFree(c->job_dev);
   cudaFreeHost(c->job_host);
   cudaFree(c->part);
-  cudaFree(c->red);
+  cudaFree(c->ticket);
   cudaFree(c->zbuf);
   cudaFree(c->aux);
   cudaFree(c->iaux);
@@ -282,23 +356,6 @@ int sr_frame_shifts(sr_ctx* c, int32_t dtype, const void* frames, int32_t nframe
   return SR_OK;
 }
 
-static int corr_partial_impl(sr_ctx* c, const sr_problem* p, double* raw) {
-  const int KP = kp_of(p->k);
-  const size_t stride = (size_t)KP * KP + 3 * KP;
-  const size_t want = stride * (size_t)c->sms * 4;
-  int rc = ensure_d(&c->part, &c->part_cap, want);
-  if (rc) return rc;
-  rc = ensure_d(&c->red, &c->red_cap, stride);
-  if (rc) return rc;
-  Args a = make_args(c, p);
-  const Launch L = launch_of(c);
-  CK(SR_SWITCH(p->dtype, p->grid.ndim, pass1, p->feature, p->param, KP, L, a, c->part, c->part_cap, c->red));
-  const int n = (int)sr_raw_size(p->k);
-  k_raw_pack<<<(n + 255) / 256, 256, 0, c->stream>>>(c->red, KP, p->k, (long long)(p->pix_hi - p->pix_lo), raw);
-  CK(cudaGetLastError());
-  return SR_OK;
-}
-
 int sr_corr_partial(sr_ctx* c, const sr_problem* p, double* raw_dev) {
   int rc = check_problem(c, p);
   if (rc) return rc;
@@ -307,18 +364,6 @@ int sr_corr_partial(sr_ctx* c, const sr_problem* p, double* raw_dev) {
   rc = upload_job(c, p, nullptr);
   if (rc) return rc;
   return corr_partial_impl(c, p, raw_dev);
-}
-
-static int finalize_impl(sr_ctx* c, const sr_problem* p, const double* raw, double h, int64_t n_total,
-                         double* stats) {
-  if (p->dtype == SR_F32)
-    k_finalize<float><<<1, 256, 0, c->stream>>>(raw, c->job_dev, p->k, p->feature, p->grid.ndim,
-                                                (double)n_total, h, (const float*)p->shifts_dev, stats);
-  else
-    k_finalize<double><<<1, 256, 0, c->stream>>>(raw, c->job_dev, p->k, p->feature, p->grid.ndim,
-                                                 (double)n_total, h, (const double*)p->shifts_dev, stats);
-  CK(cudaGetLastError());
-  return SR_OK;
 }
 
 int sr_corr_finalize(sr_ctx* c, const sr_problem* p, const double* raw_dev, const double* weights,
@@ -409,9 +454,7 @@ int sr_evaluate(sr_ctx* c, const sr_problem* p, const double* weights, double ce
   CK(cudaSetDevice(c->device));
   rc = upload_job(c, p, weights);
   if (rc) return rc;
-  rc = corr_partial_impl(c, p, raw_dev);
-  if (rc) return rc;
-  rc = finalize_impl(c, p, raw_dev, cell_volume, g.N, stats_dev);
+  rc = corr_partial_impl(c, p, raw_dev, cell_volume, stats_dev);
   if (rc) return rc;
   if (!grad_dev) return SR_OK;
   return grad_impl(c, p, stats_dev, grad_dev, p->y_off, p->param == SR_DISPLACEMENT ? p->y_stride : 0);

@@ -24,10 +24,22 @@ struct Geo {
   int n[3];
   long long N;
   long long st[3];    // flat strides (first axis fastest)
+  int sti[3];         // the same strides as int (a frame has < 2^31 cells)
   double o[3], s[3];  // origin, spacing
   double inv[3];      // 1/spacing (exact when pow2)
+  float of[3], sf[3], invf[3];  // float copies for the fp32 kernels
   int pow2;           // every spacing is a power of two
 };
+
+template <typename P> __device__ __forceinline__ P geo_o(const Geo& g, int a);
+template <> __device__ __forceinline__ float geo_o<float>(const Geo& g, int a) { return g.of[a]; }
+template <> __device__ __forceinline__ double geo_o<double>(const Geo& g, int a) { return g.o[a]; }
+template <typename P> __device__ __forceinline__ P geo_s(const Geo& g, int a);
+template <> __device__ __forceinline__ float geo_s<float>(const Geo& g, int a) { return g.sf[a]; }
+template <> __device__ __forceinline__ double geo_s<double>(const Geo& g, int a) { return g.s[a]; }
+template <typename P> __device__ __forceinline__ P geo_inv(const Geo& g, int a);
+template <> __device__ __forceinline__ float geo_inv<float>(const Geo& g, int a) { return g.invf[a]; }
+template <> __device__ __forceinline__ double geo_inv<double>(const Geo& g, int a) { return g.inv[a]; }
 
 // Per-call constants living in device memory (uploaded by the host per call).
 struct Job {
@@ -63,66 +75,92 @@ __device__ __forceinline__ double center(const Geo& g, int a, int i) {
 __device__ __forceinline__ float clampP(float t, float hi) { return fminf(fmaxf(t, 0.f), hi); }
 __device__ __forceinline__ double clampP(double t, double hi) { return fmin(fmax(t, 0.0), hi); }
 
-template <typename T, typename P, int D, bool GRAD>
+__device__ __forceinline__ float floor_to(float t) { return floorf(t); }
+__device__ __forceinline__ double floor_to(double t) { return floor(t); }
+
+// POW2: every spacing is a power of two, so (p - o) / s == (p - o) * (1/s) exactly and
+// the -0.5 can be fused (the product is exact, one rounding either way).
+template <typename T, typename P, int D, bool GRAD, bool POW2>
 __device__ __forceinline__ T interp(const T* __restrict__ img, const Geo& g, const P (&p)[D],
                                     T (&gr)[D]) {
   bool inside = true;
-  T f[D], h[D];
-  long long base = 0;
+  T f[D];
+  int base = 0;
 #pragma unroll
   for (int a = 0; a < D; ++a) {
-    P q = sub_rn(p[a], (P)g.o[a]);
-    q = g.pow2 ? mul_rn(q, (P)g.inv[a]) : div_rn(q, (P)g.s[a]);
-    const P t = sub_rn(q, (P)0.5);
+    const P q = sub_rn(p[a], geo_o<P>(g, a));
+    const P t = POW2 ? fma(q, geo_inv<P>(g, a), (P)-0.5) : sub_rn(div_rn(q, geo_s<P>(g, a)), (P)0.5);
     const P hi = (P)(g.n[a] - 1);
-    inside = inside && (t >= (P)0) && (t <= hi);
     const P tc = clampP(t, hi);  // NaN -> 0 (fmax returns the non-NaN operand)
-    int i = (int)tc;
-    i = min(i, g.n[a] - 2);
-    f[a] = (T)(tc - (P)i);
-    h[a] = (T)1 - f[a];
-    base += (long long)i * g.st[a];
+    inside = inside && (tc == t);
+    const P fl = fmin(floor_to(tc), hi - (P)1);  // min(floor(tc), n-2), exact in P
+    f[a] = (T)(tc - fl);
+    base += (int)fl * g.sti[a];
   }
-  T val = (T)0;
-  T gacc[D];
-#pragma unroll
-  for (int a = 0; a < D; ++a) gacc[a] = (T)0;
-  // corners in itertools.product((0,1), repeat=D) order: axis 0 is the slowest bit
-#pragma unroll
-  for (int c = 0; c < (1 << D); ++c) {
-    long long off = 0;
-    T w = (T)1;
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      const int ca = (c >> (D - 1 - a)) & 1;
-      off += ca ? g.st[a] : 0;
-      w *= ca ? f[a] : h[a];
-    }
-    const T v = ldg(img + base + off);
-    val += w * v;
+  const T* q0 = img + base;
+  T val;
+  T gv[D];
+  if (D == 2) {
+    const int s1 = g.sti[1];
+    const T v00 = ldg(q0), v10 = ldg(q0 + 1), v01 = ldg(q0 + s1), v11 = ldg(q0 + s1 + 1);
+    const T d0 = v10 - v00, d1 = v11 - v01;
+    const T a0 = fma(f[0], d0, v00), a1 = fma(f[0], d1, v01);
+    const T e = a1 - a0;
+    val = fma(f[1], e, a0);
     if (GRAD) {
+      gv[0] = fma(f[1], d1 - d0, d0);
+      gv[1] = e;
+    }
+  } else {
+    const int s1 = g.sti[1], s2 = g.sti[D == 3 ? 2 : 1];
+    T a[2][2], d[2][2];
 #pragma unroll
-      for (int a = 0; a < D; ++a) {
-        T dw = (T)1;
+    for (int c2 = 0; c2 < 2; ++c2)
 #pragma unroll
-        for (int b = 0; b < D; ++b) {
-          if (b == a) continue;
-          const int cb = (c >> (D - 1 - b)) & 1;
-          dw *= cb ? f[b] : h[b];
-        }
-        const int ca = (c >> (D - 1 - a)) & 1;
-        gacc[a] += ca ? dw * v : -dw * v;
+      for (int c1 = 0; c1 < 2; ++c1) {
+        const T* r = q0 + c1 * s1 + c2 * s2;
+        const T v0 = ldg(r), v1 = ldg(r + 1);
+        d[c1][c2] = v1 - v0;
+        a[c1][c2] = fma(f[0], d[c1][c2], v0);
       }
+    const T e0 = a[1][0] - a[0][0], e1 = a[1][1] - a[0][1];
+    const T b0 = fma(f[1], e0, a[0][0]), b1 = fma(f[1], e1, a[0][1]);
+    const T eb = b1 - b0;
+    val = fma(f[D - 1], eb, b0);
+    if (GRAD) {
+      const T dz0 = fma(f[1], d[1][0] - d[0][0], d[0][0]);
+      const T dz1 = fma(f[1], d[1][1] - d[0][1], d[0][1]);
+      gv[0] = fma(f[2 % D], dz1 - dz0, dz0);
+      gv[1] = fma(f[2 % D], e1 - e0, e0);
+      gv[D - 1] = eb;
     }
   }
   if (GRAD) {
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-      const T gv = g.pow2 ? gacc[a] * (T)g.inv[a] : gacc[a] / (T)g.s[a];
-      gr[a] = inside ? gv : (T)0;
+      const T gg = POW2 ? gv[a] * (T)geo_inv<P>(g, a) : gv[a] / (T)geo_s<P>(g, a);
+      gr[a] = inside ? gg : (T)0;
     }
   }
   return inside ? val : (T)0;
+}
+
+
+// ---- split multilinear sampling (2-D), used to batch the corner gathers of many samples:
+// prep: index + fractions + inside flag; fetch: the 4 corner loads; finish: the lerps.
+template <typename P, bool POW2>
+__device__ __forceinline__ void interp2_prep(const Geo& g, P px, P py, int& base, float& f0, float& f1,
+                                             bool& inside) {
+  const P q0 = sub_rn(px, geo_o<P>(g, 0)), q1 = sub_rn(py, geo_o<P>(g, 1));
+  const P t0 = POW2 ? fma(q0, geo_inv<P>(g, 0), (P)-0.5) : sub_rn(div_rn(q0, geo_s<P>(g, 0)), (P)0.5);
+  const P t1 = POW2 ? fma(q1, geo_inv<P>(g, 1), (P)-0.5) : sub_rn(div_rn(q1, geo_s<P>(g, 1)), (P)0.5);
+  const P h0 = (P)(g.n[0] - 1), h1 = (P)(g.n[1] - 1);
+  const P c0 = clampP(t0, h0), c1 = clampP(t1, h1);
+  inside = (c0 == t0) && (c1 == t1);
+  const P l0 = fmin(floor_to(c0), h0 - (P)1), l1 = fmin(floor_to(c1), h1 - (P)1);
+  f0 = (float)(c0 - l0);
+  f1 = (float)(c1 - l1);
+  base = (int)l0 + (int)l1 * g.sti[1];
 }
 
 // Flat pixel index -> integer coordinates.

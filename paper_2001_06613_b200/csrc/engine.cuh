@@ -41,6 +41,8 @@ struct Args {
   void* out;            // pass 2 output: grad (disp) / z buffer (NGF)
   long long o_off, o_stride;
   double* part_aff;     // pass 2 affine partials
+  int dbg;              // SEQREG_B200_DEBUG bits (profiling experiments only)
+  int ymap_ok;          // a y tensor map was encoded for the warp-specialized kernels
 };
 
 // --------------------------------------------------------- stats buffer layout
@@ -68,12 +70,14 @@ __host__ __device__ constexpr int pow2_floor(int x) {
 }
 
 // Pixel-tile / ownership configuration of the Gram phase of pass 1.
-template <typename T, int KP>
+template <typename T, int KP, int FEAT = NGF>
 struct G1 {
   static constexpr int RB = KP == 8 ? 2 : KP == 16 ? 4 : 8;
   static constexpr int CB = KP == 8 ? 1 : KP == 16 ? 2 : (KP == 128 && sizeof(T) == 4) ? 8 : 4;
   static constexpr int RG = KP / RB, CG = KP / CB, OWN = RG * CG;
-  static constexpr int NT = OWN > 256 ? OWN : 256;
+  // fp32 NCC with KP <= 32: 512 threads (16 warps) so each thread samples only a few
+  // frames per tile and can keep the next tile's y in flight during the Gram phase
+  static constexpr int NT = (FEAT == NCC && sizeof(T) == 4 && KP <= 32) ? 512 : (OWN > 256 ? OWN : 256);
   static constexpr int NW = NT / 32, NG = NT / OWN, OPT = RB * CB;
   static constexpr int ROWS = (32768 / (KP * (int)sizeof(T))) < 32 ? 32
                               : (32768 / (KP * (int)sizeof(T))) > 512 ? 512
@@ -88,8 +92,8 @@ struct Tile1 {
   static constexpr int R = TP * FD;
   static constexpr int RS = ((R + 31) / 32) * 32 + 4;
   static constexpr int QT = TP / 4;                            // pixel quads per tile
-  static constexpr int FPT = KP * QT / G1<T, KP>::NT;          // NCC: frames per thread
-  static constexpr int KSTEP = G1<T, KP>::NT / QT;
+  static constexpr int FPT = KP * QT / G1<T, KP, FEAT>::NT;    // NCC: frames per thread
+  static constexpr int KSTEP = G1<T, KP, FEAT>::NT / QT;
 };
 
 // Pixel-tile configuration of pass 2: a thread owns JB frames x one quad of pixels.
@@ -104,7 +108,7 @@ struct G2 {
 
 template <typename T, int D, int FEAT, int PARAM, int KP>
 constexpr size_t pass1_smem() {
-  using C = G1<T, KP>;
+  using C = G1<T, KP, FEAT>;
   using Tl = Tile1<T, D, FEAT, KP>;
   return (size_t)KP * Tl::RS * sizeof(T) + (size_t)C::OPT * C::NT * 8 + (size_t)3 * Tl::TP * 4 +
          (size_t)KP * 8 + 2 * (size_t)KP * sizeof(T) + 32;
@@ -142,17 +146,17 @@ __device__ __forceinline__ void warp_point(const Args& a, int j, long long pix, 
   }
 }
 
-template <typename T, typename P, int D, int PARAM, bool GRAD>
+template <typename T, typename P, int D, int PARAM, bool GRAD, bool POW2>
 __device__ __forceinline__ T sample_at(const Args& a, const T* img, int j, long long pix,
                                        const int (&c)[3], T (&gr)[D]) {
   P p[D];
   warp_point<T, P, D, PARAM>(a, j, pix, c, p);
-  return interp<T, P, D, GRAD>(img, a.g, p, gr);
+  return interp<T, P, D, GRAD, POW2>(img, a.g, p, gr);
 }
 
 // Four consecutive pixels p0..p0+3 (nvalid of them inside the slab) of subset frame j.
 // Displacement: the y quads are one 16-byte load per component when aligned.
-template <typename T, typename P, int D, int PARAM, bool GRAD>
+template <typename T, typename P, int D, int PARAM, bool GRAD, bool POW2>
 __device__ __forceinline__ void sample_quad(const Args& a, const T* img, int j, long long p0, int nvalid,
                                             bool vec, const int* crd4, T (&v)[4], T (&gr)[4][D]) {
   P p[4][D];
@@ -179,16 +183,46 @@ __device__ __forceinline__ void sample_quad(const Args& a, const T* img, int j, 
     }
   }
 #pragma unroll
-  for (int e = 0; e < 4; ++e) v[e] = interp<T, P, D, GRAD>(img, a.g, p[e], gr[e]);
+  for (int e = 0; e < 4; ++e) v[e] = interp<T, P, D, GRAD, POW2>(img, a.g, p[e], gr[e]);
+}
+
+// Interpolate four prepared points (the quad's y already in registers).
+template <typename T, typename P, int D, bool GRAD, bool POW2>
+__device__ __forceinline__ void sample_pts4(const T* img, const Geo& g, const T (&yq)[D][4], T (&v)[4],
+                                            T (&gr)[4][D]) {
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    P p[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) p[c] = (P)yq[c][e];
+    v[e] = interp<T, P, D, GRAD, POW2>(img, g, p, gr[e]);
+  }
+}
+
+// Load the quad's y (all components) of subset frame j: 16-byte loads when aligned.
+template <typename T, int D>
+__device__ __forceinline__ void load_yq(const Args& a, int j, long long p0, int nvalid, bool vec,
+                                        T (&yq)[D][4]) {
+  const T* y = reinterpret_cast<const T*>(a.y) + (p0 - a.y_off);
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    const T* yc = y + (long long)(j * D + c) * a.y_stride;
+    if (vec) {
+      ldg4(yc, yq[c]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) yq[c][e] = e < nvalid ? ldg(yc + e) : (T)0;
+    }
+  }
 }
 
 // NGF feature at one pixel: u = T_j(y_j) on the cell centres, p = grad_h u (central
 // differences, one-sided at the domain edge), rho = sqrt(|p|^2 + eps^2), n = p / rho.
-template <typename T, typename P, int D, int PARAM>
+template <typename T, typename P, int D, int PARAM, bool POW2>
 __device__ __forceinline__ void ngf_at(const Args& a, const T* img, int j, long long pix,
                                        const int (&c)[3], T (&n)[D], T& rho) {
   T dummy[D];
-  const T u0 = sample_at<T, P, D, PARAM, false>(a, img, j, pix, c, dummy);
+  const T u0 = sample_at<T, P, D, PARAM, false, POW2>(a, img, j, pix, c, dummy);
   T up[D], um[D];
 #pragma unroll
   for (int ax = 0; ax < D; ++ax) {
@@ -196,8 +230,8 @@ __device__ __forceinline__ void ngf_at(const Args& a, const T* img, int j, long 
     int cp[3] = {c[0], c[1], c[2]}, cm[3] = {c[0], c[1], c[2]};
     cp[ax] += hp ? 1 : 0;
     cm[ax] -= hm ? 1 : 0;
-    up[ax] = sample_at<T, P, D, PARAM, false>(a, img, j, pix + (hp ? a.g.st[ax] : 0), cp, dummy);
-    um[ax] = sample_at<T, P, D, PARAM, false>(a, img, j, pix - (hm ? a.g.st[ax] : 0), cm, dummy);
+    up[ax] = sample_at<T, P, D, PARAM, false, POW2>(a, img, j, pix + (hp ? a.g.st[ax] : 0), cp, dummy);
+    um[ax] = sample_at<T, P, D, PARAM, false, POW2>(a, img, j, pix - (hm ? a.g.st[ax] : 0), cm, dummy);
   }
   T pn = (T)0;
 #pragma unroll
@@ -224,9 +258,9 @@ __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
 }
 
 // ===================================================================== pass 1
-template <typename T, int D, int FEAT, int PARAM, int KP>
-__global__ void __launch_bounds__(G1<T, KP>::NT) k_pass1(const Args a) {
-  using C = G1<T, KP>;
+template <typename T, int D, int FEAT, int PARAM, int KP, bool POW2>
+__device__ __forceinline__ void pass1_body(const Args& a) {
+  using C = G1<T, KP, FEAT>;
   using Tl = Tile1<T, D, FEAT, KP>;
   using P = typename std::conditional<PARAM == AFFINE, double, T>::type;
   constexpr int TP = Tl::TP, R = Tl::R, RS = Tl::RS, NT = C::NT;
@@ -264,11 +298,11 @@ __global__ void __launch_bounds__(G1<T, KP>::NT) k_pass1(const Args a) {
 
   // NCC per-thread running sum / max / min of its fixed frame set (k = kb + KSTEP*i)
   const int q = tid % QT, kb = tid / QT;
-  double fsum[FEAT == NCC ? FPT : 1];
+  T fsum[FEAT == NCC ? FPT : 1];
   T fmx[FEAT == NCC ? FPT : 1], fmn[FEAT == NCC ? FPT : 1];
 #pragma unroll
   for (int i = 0; i < (FEAT == NCC ? FPT : 1); ++i) {
-    fsum[i] = 0.0;
+    fsum[i] = (T)0;
     fmx[i] = -INFINITY;
     fmn[i] = INFINITY;
   }
@@ -279,6 +313,8 @@ __global__ void __launch_bounds__(G1<T, KP>::NT) k_pass1(const Args a) {
   const long long ntiles = (npix + TP - 1) / TP;
   const bool yvec = PARAM == DISP && (a.y_stride % 4 == 0) &&
                     ((reinterpret_cast<uintptr_t>(a.y) & 15) == 0);
+  T ypf[(FEAT == NCC && PARAM == DISP) ? FPT : 1][D][4];
+  bool first = true;
 
   for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const long long t0 = a.pix_lo + tile * TP;
@@ -293,11 +329,20 @@ __global__ void __launch_bounds__(G1<T, KP>::NT) k_pass1(const Args a) {
       __syncthreads();
     }
     if (FEAT == NCC) {
-      // ---- sampling: thread -> one pixel quad of FPT frames; all loads of a quad in flight
+      // ---- sampling: thread -> one pixel quad of FPT frames; the quad's y was prefetched
+      // during the previous tile's Gram phase (displacement), so only the gathers wait
       const long long p0 = t0 + 4 * q;
       const long long nv = a.pix_hi - p0;
       const int nvalid = nv >= 4 ? 4 : (nv > 0 ? (int)nv : 0);
-      const bool vec = yvec && nvalid == 4 && (((p0 - a.y_off) & 3) == 0);
+      if (PARAM == DISP && first) {
+        const bool vec = yvec && nvalid == 4 && (((p0 - a.y_off) & 3) == 0);
+#pragma unroll
+        for (int i = 0; i < FPT; ++i) {
+          const int k = kb + KSTEP * i;
+          if (k < K) load_yq<T, D>(a, k, p0, nvalid, vec, ypf[PARAM == DISP ? i : 0]);
+        }
+      }
+      first = false;
 #pragma unroll
       for (int i = 0; i < FPT; ++i) {
         const int k = kb + KSTEP * i;
@@ -306,17 +351,33 @@ __global__ void __launch_bounds__(G1<T, KP>::NT) k_pass1(const Args a) {
           const T* img = frames + (long long)fi * a.g.N;
           const T sh = shifts ? shifts[fi] : (T)0;
           T v[4], gr[4][D];
-          sample_quad<T, P, D, PARAM, false>(a, img, k, p0, nvalid, vec, crd + 12 * q, v, gr);
+          if (PARAM == DISP) sample_pts4<T, P, D, false, POW2>(img, a.g, ypf[PARAM == DISP ? i : 0], v, gr);
+          else sample_quad<T, P, D, PARAM, false, POW2>(a, img, k, p0, nvalid, false, crd + 12 * q, v, gr);
           T out[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const bool ok = e < nvalid;
             out[e] = ok ? v[e] - sh : (T)0;
-            fsum[i] += (double)out[e];
+            fsum[i] += out[e];
             fmx[i] = ok ? max(fmx[i], v[e]) : fmx[i];
             fmn[i] = ok ? min(fmn[i], v[e]) : fmn[i];
           }
           sts4(V + (size_t)k * RS + 4 * q, out);
+        }
+      }
+      if (PARAM == DISP) {
+        // prefetch the next tile's y: in flight while this tile's Gram runs
+        const long long nt = tile + gridDim.x;
+        if (nt < ntiles) {
+          const long long p1 = a.pix_lo + nt * TP + 4 * q;
+          const long long nv1 = a.pix_hi - p1;
+          const int nval1 = nv1 >= 4 ? 4 : (nv1 > 0 ? (int)nv1 : 0);
+          const bool vec1 = yvec && nval1 == 4 && (((p1 - a.y_off) & 3) == 0);
+#pragma unroll
+          for (int i = 0; i < FPT; ++i) {
+            const int k = kb + KSTEP * i;
+            if (k < K) load_yq<T, D>(a, k, p1, nval1, vec1, ypf[PARAM == DISP ? i : 0]);
+          }
         }
       }
     } else {
@@ -337,7 +398,7 @@ __global__ void __launch_bounds__(G1<T, KP>::NT) k_pass1(const Args a) {
           const T* img = frames + (long long)fi * a.g.N;
           const int c[3] = {crd[3 * pp], crd[3 * pp + 1], crd[3 * pp + 2]};
           T rho;
-          ngf_at<T, P, D, PARAM>(a, img, k, pix, c, n, rho);
+          ngf_at<T, P, D, PARAM, POW2>(a, img, k, pix, c, n, rho);
         } else {
 #pragma unroll
           for (int cc = 0; cc < D; ++cc) n[cc] = (T)0;
@@ -352,7 +413,7 @@ __global__ void __launch_bounds__(G1<T, KP>::NT) k_pass1(const Args a) {
     }
     __syncthreads();
     // ---- Gram: each owner accumulates an RB x CB block over its row quads
-#pragma unroll 2
+#pragma unroll 1
     for (int qq = grp; qq < R / 4; qq += NG) {
       T rv[RB][4], cv[CB][4];
 #pragma unroll
@@ -398,7 +459,7 @@ __global__ void __launch_bounds__(G1<T, KP>::NT) k_pass1(const Args a) {
 #pragma unroll
     for (int i = 0; i < FPT; ++i) {
       const int k = kb + KSTEP * i;
-      rs[(size_t)k * QT + q] = fsum[i];
+      rs[(size_t)k * QT + q] = (double)fsum[i];
       rmx[(size_t)k * QT + q] = fmx[i];
       rmn[(size_t)k * QT + q] = fmn[i];
     }
@@ -424,9 +485,15 @@ __global__ void __launch_bounds__(G1<T, KP>::NT) k_pass1(const Args a) {
   }
 }
 
-// Fixed-order reduction of per-CTA partials: block handles 32 consecutive elements,
-// warp w sums CTAs w, w+8, ...; then warp 0 combines the 8 warp sums in order.
-// Elements in [n_sum, n_max_end) are max-reduced, the rest summed.
+template <typename T, int D, int FEAT, int PARAM, int KP>
+__global__ void __launch_bounds__(G1<T, KP, FEAT>::NT) k_pass1(const Args a) {
+  if (a.g.pow2) pass1_body<T, D, FEAT, PARAM, KP, true>(a);
+  else pass1_body<T, D, FEAT, PARAM, KP, false>(a);
+}
+
+// Fixed-order reduction of per-CTA partials (used for small partial sets, e.g. S(y)):
+// block handles 32 consecutive elements, warp w sums CTAs w, w+8, ...; warp 0 combines
+// the 8 warp sums in order.  Elements in [n_sum, n_max_end) are max-reduced.
 static __global__ void __launch_bounds__(256) k_reduce(const double* __restrict__ part, int nblk,
                                                        int stride, int n_sum, int n_max_end, int n_total,
                                                        double* __restrict__ red) {
@@ -450,60 +517,48 @@ static __global__ void __launch_bounds__(256) k_reduce(const double* __restrict_
   }
 }
 
-// Scatter the KP-padded reduced vector into the caller's raw layout
-// [G k*k | s k | vmax k | -vmin k | count].
-static __global__ void k_raw_pack(const double* __restrict__ red, int KP, int K, long long count,
-                                  double* __restrict__ raw) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < K * K) {
-    const int i = t / K, j = t % K;
-    raw[t] = red[i * KP + j];
-  } else if (t < K * K + 3 * K) {
-    const int blk = (t - K * K) / K, k = (t - K * K) % K;
-    raw[t] = red[KP * KP + blk * KP + k];
-  } else if (t == K * K + 3 * K) {
-    raw[t] = (double)count;
-  }
-}
-
 // ==================================================================== finalize
-// One CTA.  raw = [G | s | vmax | -vmin | count] (all-reduced when sharded).
+// Block-level finalize (any blockDim that is a power of two, <= 1024).  raw = [G | s | vmax |
+// -vmin | count] (all-reduced when sharded), read with ld.global.cg (it may have just been
+// written by other CTAs of the same grid).  Cmat: dynamic shared memory of K*K doubles.
 template <typename T>
-__global__ void __launch_bounds__(256) k_finalize(const double* __restrict__ raw, const Job* job,
-                                                  int K, int feat, int D, double n_total,
-                                                  double h, const T* shifts,
-                                                  double* __restrict__ stats) {
-  __shared__ double sig[kMaxFrames], mu[kMaxFrames], w[kMaxFrames], cj[kMaxFrames];
+__device__ void finalize_block(const double* __restrict__ raw, const Job* job, int K, int feat, int D,
+                               double n_total, double h, const T* shifts, double* __restrict__ stats,
+                               double* Cmat) {
+  __shared__ double sig[kMaxFrames], isg[kMaxFrames], mu[kMaxFrames], w[kMaxFrames], cj[kMaxFrames],
+      sv[kMaxFrames];
   __shared__ int deg[kMaxFrames];
-  __shared__ double red[256];
-  const int tid = threadIdx.x;
+  __shared__ double red[1024];
+  const int tid = threadIdx.x, nt = blockDim.x;
   const StatsLayout L(K);
   const double* G = raw;
-  const double* s = raw + K * K;
-  const double* vmx = raw + K * K + K;
-  const double* vmnn = raw + K * K + 2 * K;
   const double N = n_total;
   if (tid < K) {
-    const double gii = G[tid * K + tid];
-    const double amax = fmax(vmx[tid], vmnn[tid]);  // max |v|
+    const double gii = __ldcg(G + tid * K + tid);
+    const double si = __ldcg(raw + K * K + tid);
+    const double vmx = __ldcg(raw + K * K + K + tid), vmnn = __ldcg(raw + K * K + 2 * K + tid);
+    const double amax = fmax(vmx, vmnn);  // max |v|
     double sg, m = 0.0, thr;
     int dg;
     if (feat == NCC) {
-      m = s[tid] / N;
-      const double var = gii - s[tid] * m;
+      m = si / N;
+      const double var = gii - si * m;
       sg = sqrt(fmax(var, 0.0));
       thr = 1e-12 * sqrt(N) * (1.0 + amax);  // similarity.py:84-86
       // an exactly constant frame has centred norm 0 in the reference; the raw-moment
       // form cannot see that through cancellation, the extrema can
-      dg = !(sg >= thr) || (vmx[tid] == -vmnn[tid]);
-      if (vmx[tid] == -vmnn[tid]) sg = 0.0;
+      const bool constant = vmx == -vmnn;
+      dg = !(sg >= thr) || constant;
+      if (constant) sg = 0.0;
     } else {
       sg = sqrt(fmax(gii, 0.0));
       thr = 1e-12 * sqrt(N * D) * (1.0 + amax);
       dg = !(sg >= thr);
     }
     sig[tid] = sg;
+    isg[tid] = dg ? 0.0 : 1.0 / sg;
     mu[tid] = m;
+    sv[tid] = si;
     deg[tid] = dg;
     w[tid] = job->weights[tid];
     const double sh = (feat == NCC && shifts) ? (double)shifts[job->frame_index[tid]] : 0.0;
@@ -516,29 +571,39 @@ __global__ void __launch_bounds__(256) k_finalize(const double* __restrict__ raw
   }
   __syncthreads();
   // C (upper triangle computed once, mirrored -> exactly symmetric, similarity.py:155)
-  for (int e = tid; e < K * K; e += 256) {
+  for (int e = tid; e < K * K; e += nt) {
     const int i = e / K, j = e % K;
     if (i > j) continue;
     double c = 0.0;
     if (!deg[i] && !deg[j]) {
-      const double num = feat == NCC ? G[i * K + j] - s[i] * mu[j] : G[i * K + j];
-      c = num / (sig[i] * sig[j]);
+      const double gij = __ldcg(G + i * K + j);
+      const double num = feat == NCC ? gij - sv[i] * mu[j] : gij;
+      c = num * (isg[i] * isg[j]);
     }
-    stats[L.C + i * K + j] = c;
-    stats[L.C + j * K + i] = c;
+    Cmat[i * K + j] = c;
+    Cmat[j * K + i] = c;
   }
   __syncthreads();
   // D = h * [(sum w)^2 - sum w^2 - sum_{i != j} w_i w_j C_ij^2]   (similarity.py:167-177)
   double part = 0.0;
-  for (int e = tid; e < K * K; e += 256) {
+  for (int e = tid; e < K * K; e += nt) {
     const int i = e / K, j = e % K;
-    if (i == j) continue;
-    const double c = stats[L.C + e];
-    part += w[i] * w[j] * c * c;
+    const double c = Cmat[e];
+    stats[L.C + e] = c;
+    if (i != j) part += w[i] * w[j] * c * c;
   }
   red[tid] = part;
+  // c_j = sum_i w_i C_ij^2  (= f_j . g_j, similarity.py:210)
+  if (tid < K) {
+    double c = 0.0;
+    for (int i = 0; i < K; ++i) {
+      const double v = Cmat[i * K + tid];
+      c += w[i] * v * v;
+    }
+    cj[tid] = c;
+  }
   __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
+  for (int o = nt / 2; o > 0; o >>= 1) {
     if (tid < o) red[tid] += red[tid + o];
     __syncthreads();
   }
@@ -554,36 +619,97 @@ __global__ void __launch_bounds__(256) k_finalize(const double* __restrict__ raw
     stats[2] = N;
     stats[3] = h;
   }
-  // c_j = sum_i w_i C_ij^2  (= f_j . g_j, similarity.py:210)
-  if (tid < K) {
-    double c = 0.0;
-    for (int i = 0; i < K; ++i) {
-      const double v = stats[L.C + i * K + tid];
-      c += w[i] * v * v;
-    }
-    cj[tid] = c;
-  }
-  __syncthreads();
-  // M'_ij = -4 h w_j (w_i C_ij / sig_i - delta_ij c_j / sig_j) / sig_j
+  // M'_ij = -4 h w_j (w_i C_ij / sig_i - delta_ij c_j / sig_j) / sig_j ;  beta'_j = -sum_i M'_ij mu_i
   float* Mf = reinterpret_cast<float*>(stats + L.Mf);
-  for (int e = tid; e < K * K; e += 256) {
+  for (int e = tid; e < K * K; e += nt) {
     const int i = e / K, j = e % K;
     double m = 0.0;
     if (!deg[i] && !deg[j]) {
-      double t = w[i] * stats[L.C + e] / sig[i];
-      if (i == j) t -= cj[j] / sig[j];
-      m = -4.0 * h * w[j] * t / sig[j];
+      double t = w[i] * Cmat[e] * isg[i];
+      if (i == j) t -= cj[j] * isg[j];
+      m = -4.0 * h * w[j] * t * isg[j];
     }
     stats[L.M + e] = m;
     Mf[e] = (float)m;
   }
-  __syncthreads();
   if (tid < K) {
+    const int j = tid;
     double b = 0.0;
-    if (feat == NCC)
-      for (int i = 0; i < K; ++i) b -= stats[L.M + i * K + tid] * mu[i];
-    stats[L.beta + tid] = b;
+    if (feat == NCC && !deg[j]) {
+      const double aj = -4.0 * h * w[j] * isg[j];
+      for (int i = 0; i < K; ++i) {
+        if (deg[i]) continue;
+        double t = w[i] * Cmat[i * K + j] * isg[i];
+        if (i == j) t -= cj[j] * isg[j];
+        b -= aj * t * mu[i];
+      }
+    }
+    stats[L.beta + j] = b;
   }
+}
+
+// Cross-CTA reduction of the pass-1 partials (fixed order: warp w of a block sums CTAs
+// w, w+32, ..., then warp 0 combines the 32 warp sums in order) packed straight into the
+// caller's raw layout; the last block to finish (atomic ticket) writes the count and, when
+// asked, runs the finalize on the complete raw sums.  One launch instead of three.
+template <typename T>
+__global__ void __launch_bounds__(1024) k_reduce_finalize(const double* __restrict__ part, int nblk, int KP,
+                                                          int K, long long count, double* raw, int do_final,
+                                                          const Job* job, int feat, int D, double h,
+                                                          const T* shifts, double* stats,
+                                                          unsigned* ticket) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  __shared__ double buf[32][33];
+  __shared__ int is_last;
+  const int stride = KP * KP + 3 * KP;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int e = blockIdx.x * 32 + lane;
+  const bool is_max = e >= KP * KP + KP && e < stride;
+  double acc = is_max ? -INFINITY : 0.0;
+  if (e < stride) {
+    int b = warp;
+#pragma unroll 4
+    for (; b < nblk; b += 32) {
+      const double v = __ldcg(part + (size_t)b * stride + e);
+      acc = is_max ? fmax(acc, v) : acc + v;
+    }
+  }
+  buf[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && e < stride) {
+    double s = buf[0][lane];
+    for (int w2 = 1; w2 < 32; ++w2) s = is_max ? fmax(s, buf[w2][lane]) : s + buf[w2][lane];
+    int r = -1;
+    if (e < KP * KP) {
+      const int i = e / KP, j = e % KP;
+      if (i < K && j < K) r = i * K + j;
+    } else {
+      const int blk = (e - KP * KP) / KP, k = (e - KP * KP) % KP;
+      if (k < K) r = K * K + blk * K + k;
+    }
+    if (r >= 0) raw[r] = s;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  if (threadIdx.x == 0) {
+    raw[K * K + 3 * K] = (double)count;
+    *ticket = 0u;
+  }
+  if (!do_final) return;
+  finalize_block<T>(raw, job, K, feat, D, (double)count, h, shifts, stats, reinterpret_cast<double*>(dsm));
+}
+
+// Finalize only (sharded path: raw sums all-reduced by the caller).
+template <typename T>
+__global__ void __launch_bounds__(1024) k_finalize(const double* __restrict__ raw, const Job* job, int K,
+                                                   int feat, int D, double n_total, double h,
+                                                   const T* shifts, double* __restrict__ stats) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  finalize_block<T>(raw, job, K, feat, D, n_total, h, shifts, stats, reinterpret_cast<double*>(dsm));
 }
 
 // ===================================================================== pass 2
@@ -599,8 +725,8 @@ __device__ __forceinline__ const double* coef_ptr<double>(const double* stats,
   return stats + L.M;
 }
 
-template <typename T, int D, int FEAT, int PARAM, int KP>
-__global__ void __launch_bounds__(G2<T, KP>::NT) k_pass2(const Args a) {
+template <typename T, int D, int FEAT, int PARAM, int KP, bool POW2>
+__device__ __forceinline__ void pass2_body(const Args& a) {
   using C = G2<T, KP>;
   using P = typename std::conditional<PARAM == AFFINE, double, T>::type;
   constexpr int TP = C::TP, TS = C::TS, NT = C::NT, JB = C::JB, QN = C::QN;
@@ -680,7 +806,7 @@ __global__ void __launch_bounds__(G2<T, KP>::NT) k_pass2(const Args a) {
           const T* img = frames + (long long)fi * a.g.N;
           const T sh = shifts ? shifts[fi] : (T)0;
           T v[4], gr[4][D];
-          sample_quad<T, P, D, PARAM, true>(a, img, k, p0, nvalid, vec, crd + 12 * qd, v, gr);
+          sample_quad<T, P, D, PARAM, true, POW2>(a, img, k, p0, nvalid, vec, crd + 12 * qd, v, gr);
           T o4[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) o4[e] = e < nvalid ? v[e] - sh : (T)0;
@@ -702,7 +828,7 @@ __global__ void __launch_bounds__(G2<T, KP>::NT) k_pass2(const Args a) {
           const int fi = a.job->frame_index[k];
           const T* img = frames + (long long)fi * a.g.N;
           const int c[3] = {crd[3 * pp], crd[3 * pp + 1], crd[3 * pp + 2]};
-          ngf_at<T, P, D, PARAM>(a, img, k, pix, c, n, rho);
+          ngf_at<T, P, D, PARAM, POW2>(a, img, k, pix, c, n, rho);
         } else {
           rho = (T)1;
 #pragma unroll
@@ -839,6 +965,14 @@ __global__ void __launch_bounds__(G2<T, KP>::NT) k_pass2(const Args a) {
   }
 }
 
+template <typename T, int D, int FEAT, int PARAM, int KP>
+__global__ void __launch_bounds__(G2<T, KP>::NT) k_pass2(const Args a) {
+  if (a.g.pow2) pass2_body<T, D, FEAT, PARAM, KP, true>(a);
+  else pass2_body<T, D, FEAT, PARAM, KP, false>(a);
+}
+
+// NGF second half of pass 2: dD/du_j = sum_a Dx_a^T z_{j,a}, then dD/dy_j = dD/du_j grad T_j(y_j).
+// Adjoint of the central/one-sided difference.
 template <typename T, int D>
 __device__ __forceinline__ T dgrad_adjoint(const T* __restrict__ z, long long idx, long long st,
                                            int i, int n, T inv) {
@@ -854,9 +988,9 @@ __device__ __forceinline__ T dgrad_adjoint(const T* __restrict__ z, long long id
   return out;
 }
 
-template <typename T, int D, int PARAM>
-__global__ void __launch_bounds__(256) k_ngf_adjoint(const Args a, const T* __restrict__ zb,
-                                                     long long z_off, long long z_stride) {
+template <typename T, int D, int PARAM, bool POW2>
+__device__ __forceinline__ void ngf_adjoint_body(const Args& a, const T* __restrict__ zb,
+                                                 long long z_off, long long z_stride) {
   using P = typename std::conditional<PARAM == AFFINE, double, T>::type;
   constexpr int NA = D * (D + 1);
   const int j = blockIdx.y;
@@ -876,7 +1010,7 @@ __global__ void __launch_bounds__(256) k_ngf_adjoint(const Args a, const T* __re
     const int fi = a.job->frame_index[j];
     const T* img = reinterpret_cast<const T*>(a.frames) + (long long)fi * a.g.N;
     T gr[D];
-    sample_at<T, P, D, PARAM, true>(a, img, j, pix, c, gr);
+    sample_at<T, P, D, PARAM, true, POW2>(a, img, j, pix, c, gr);
     if (PARAM == DISP) {
       T* out = reinterpret_cast<T*>(a.out);
 #pragma unroll
@@ -910,6 +1044,13 @@ __global__ void __launch_bounds__(256) k_ngf_adjoint(const Args a, const T* __re
       a.part_aff[((size_t)j * gridDim.x + blockIdx.x) * NA + threadIdx.x] = s;
     }
   }
+}
+
+template <typename T, int D, int PARAM>
+__global__ void __launch_bounds__(256) k_ngf_adjoint(const Args a, const T* __restrict__ zb,
+                                                     long long z_off, long long z_stride) {
+  if (a.g.pow2) ngf_adjoint_body<T, D, PARAM, true>(a, zb, z_off, z_stride);
+  else ngf_adjoint_body<T, D, PARAM, false>(a, zb, z_off, z_stride);
 }
 
 // Gather affine partials [nblk][KP][NA] (pass 2 NCC) or [K][nblk][NA] (NGF) into rows
@@ -1064,3 +1205,5 @@ __global__ void __launch_bounds__(256) k_frame_mean(const T* __restrict__ frames
 }
 
 }  // namespace sr
+
+#include "engine_ws.cuh"

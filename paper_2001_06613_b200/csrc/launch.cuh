@@ -2,14 +2,52 @@
 // Included by the per-(dtype, ndim) instantiation units inst_*.cu.
 #pragma once
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <cuda.h>
 #include "engine.cuh"
 
 namespace sr {
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda needed)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2-D view of the displacement planes: rows = k*D + c (K*D of them), columns = pixels of the
+// y buffer; boxes of `box_cols` pixels x all rows.
+template <typename T>
+static bool encode_y_map(CUtensorMap* m, const Args& a, int rows, int box_cols) {
+  EncodeTiledFn fn = encode_tiled_fn();
+  if (!fn || (reinterpret_cast<uintptr_t>(a.y) & 15) || ((a.y_stride * (long long)sizeof(T)) % 16) || rows > 256)
+    return false;
+  cuuint64_t gdim[2] = {(cuuint64_t)a.y_stride, (cuuint64_t)rows};
+  cuuint64_t gstr[1] = {(cuuint64_t)a.y_stride * sizeof(T)};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)rows};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+            const_cast<void*>(a.y), gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 struct Launch {
   cudaStream_t stream;
   int sms;
   int grid_override;  // 0 = auto
+  int legacy;         // 1 = force the non-specialized kernels (A/B checks)
 };
 
 template <typename K>
@@ -26,10 +64,13 @@ static int occupancy_grid(const Launch& L, K kernel, int nt, size_t smem, long l
 
 template <typename T, int D, int FEAT, int PARAM, int KP>
 struct Runner {
-  // pass 1 + cross-CTA reduce; returns number of CTAs used, writes red[KP*KP+2KP]
+  // pass 1; per-CTA partials [grid][KP*KP + 3KP] in `part`, CTA count in *nblk
   static cudaError_t pass1(const Launch& L, const Args& a, double* part, size_t part_cap,
-                           double* red) {
-    using C = G1<T, KP>;
+                           int* nblk) {
+    if constexpr (FEAT == NCC && PARAM == DISP && KP <= 32) {
+      if (!L.legacy) return pass1_ws(L, a, part, part_cap, nblk);
+    }
+    using C = G1<T, KP, FEAT>;
     using Tl = Tile1<T, D, FEAT, KP>;
     const size_t smem = pass1_smem<T, D, FEAT, PARAM, KP>();
     auto kern = k_pass1<T, D, FEAT, PARAM, KP>;
@@ -43,9 +84,31 @@ struct Runner {
     Args b = a;
     b.part = part;
     kern<<<grid, C::NT, smem, L.stream>>>(b);
-    const int n_total = (int)stride;
-    k_reduce<<<(n_total + 31) / 32, 256, 0, L.stream>>>(part, grid, (int)stride, KP * KP + KP,
-                                                          KP * KP + 3 * KP, n_total, red);
+    *nblk = grid;
+    return cudaGetLastError();
+  }
+
+  // warp-specialized pass 1 (NCC displacement, KP <= 32), engine_ws.cuh
+  static cudaError_t pass1_ws(const Launch& L, const Args& a, double* part, size_t part_cap, int* nblk) {
+    using C = WS1<T, KP>;
+    const size_t smem = ws1_smem<T, D, KP>();
+    auto kern = k_pass1_ws<T, D, KP>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const long long npix = a.pix_hi - a.pix_lo;
+    const long long ntiles = (npix + C::TP - 1) / C::TP;
+    int grid = occupancy_grid(L, kern, C::NT, smem, ntiles > 0 ? ntiles : 1);
+    const size_t stride = (size_t)KP * KP + 3 * KP;
+    if ((size_t)grid * stride > part_cap) grid = (int)(part_cap / stride);
+    Args b = a;
+    b.part = part;
+    CUtensorMap ymap;
+    memset(&ymap, 0, sizeof ymap);
+    b.ymap_ok = encode_y_map<T>(&ymap, a, a.K * D, C::TP) ? 1 : 0;
+    if (getenv("SEQREG_B200_TRACE"))
+      fprintf(stderr, "[seqreg_b200] pass1_ws grid=%d smem=%zu dbg=%d ymap_ok=%d\n", grid, smem, b.dbg, b.ymap_ok);
+    kern<<<grid, C::NT, smem, L.stream>>>(b, ymap);
+    *nblk = grid;
     return cudaGetLastError();
   }
 
@@ -105,7 +168,7 @@ cudaError_t run_curvature(const Launch& L, const Args& a, double alpha, double h
 template <typename T, int D>
 struct Dispatch {
   template <int FEAT, int PARAM>
-  static cudaError_t p1k(int KP, const Launch& L, const Args& a, double* part, size_t cap, double* red) {
+  static cudaError_t p1k(int KP, const Launch& L, const Args& a, double* part, size_t cap, int* red) {
     switch (KP) {
       case 8: return Runner<T, D, FEAT, PARAM, 8>::pass1(L, a, part, cap, red);
       case 16: return Runner<T, D, FEAT, PARAM, 16>::pass1(L, a, part, cap, red);
@@ -125,7 +188,7 @@ struct Dispatch {
     }
   }
   static cudaError_t pass1(int feat, int param, int KP, const Launch& L, const Args& a,
-                           double* part, size_t cap, double* red) {
+                           double* part, size_t cap, int* red) {
     if (feat == NCC) return param == AFFINE ? p1k<NCC, AFFINE>(KP, L, a, part, cap, red)
                                             : p1k<NCC, DISP>(KP, L, a, part, cap, red);
     return param == AFFINE ? p1k<NGF, AFFINE>(KP, L, a, part, cap, red)
@@ -153,7 +216,7 @@ struct Dispatch {
 // Entry points implemented in inst_<dtype>_d<D>.cu
 #define SR_DECLARE_INST(TT, DD)                                                               \
   cudaError_t pass1_##TT##_d##DD(int feat, int param, int KP, const Launch& L, const Args& a, \
-                                 double* part, size_t cap, double* red);                     \
+                                 double* part, size_t cap, int* red);                        \
   cudaError_t pass2_##TT##_d##DD(int feat, int param, int KP, const Launch& L, const Args& a, \
                                  double* pa, size_t cap, int* nb);                           \
   cudaError_t adjoint_##TT##_d##DD(int param, const Launch& L, const Args& a, const void* zb, \
@@ -163,7 +226,7 @@ struct Dispatch {
 
 #define SR_DEFINE_INST(TT, T, DD)                                                             \
   cudaError_t pass1_##TT##_d##DD(int feat, int param, int KP, const Launch& L, const Args& a, \
-                                 double* part, size_t cap, double* red) {                    \
+                                 double* part, size_t cap, int* red) {                       \
     return Dispatch<T, DD>::pass1(feat, param, KP, L, a, part, cap, red);                     \
   }                                                                                           \
   cudaError_t pass2_##TT##_d##DD(int feat, int param, int KP, const Launch& L, const Args& a, \
