@@ -14,6 +14,15 @@
 
 using namespace sr;
 
+// fp32 frame stacks copied into gather-capable CUDA arrays (sr_frames_prepare)
+struct TexSet {
+  const void* ptr = nullptr;
+  int nframes = 0;
+  long long N = 0;
+  std::vector<cudaArray_t> arr;
+  std::vector<cudaTextureObject_t> tex;
+};
+
 struct sr_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -21,6 +30,8 @@ struct sr_ctx {
   int grid_override = 0;
   int legacy = 0;  // SEQREG_B200_LEGACY=1: non-specialized kernels only
   int dbg = 0;     // SEQREG_B200_DEBUG: profiling experiment bits
+  int ws2 = 0;     // SEQREG_B200_WS2=1: warp-specialized pass 2
+  int tex_enabled = 0;  // SEQREG_B200_TEX=1: texture-gather sampling (measured slower on B200)
   Job* job_dev = nullptr;
   Job* job_host = nullptr;  // pinned staging
   Job job_last{};           // content of the last upload (skip identical re-uploads)
@@ -34,7 +45,22 @@ struct sr_ctx {
   size_t aux_cap = 0;
   int* iaux = nullptr;
   size_t iaux_cap = 0;
+  std::vector<TexSet> texsets;
+  int job_use_tex = 0;  // the uploaded job carries texture handles
 };
+
+static void texset_free(TexSet& t) {
+  for (auto o : t.tex) cudaDestroyTextureObject(o);
+  for (auto a : t.arr) cudaFreeArray(a);
+  t.tex.clear();
+  t.arr.clear();
+}
+
+static const TexSet* texset_find(sr_ctx* c, const void* ptr, int nframes, long long N) {
+  for (auto& t : c->texsets)
+    if (t.ptr == ptr && t.nframes == nframes && t.N == N) return &t;
+  return nullptr;
+}
 
 static thread_local std::string g_err;
 
@@ -165,6 +191,7 @@ static Args make_args(sr_ctx* ctx, const sr_problem* p) {
   a.pix_hi = p->pix_hi;
   a.eps = p->ngf_eps;
   a.dbg = ctx->dbg;
+  a.use_tex = ctx->job_use_tex;
   return a;
 }
 
@@ -182,6 +209,13 @@ static int upload_job(sr_ctx* ctx, const sr_problem* p, const double* weights) {
     for (int j = 0; j < p->k; ++j)
       for (int e = 0; e < na; ++e) nj.affine[j * 12 + e] = p->affine[j * na + e];
   }
+  {
+    long long N = 1;
+    for (int a2 = 0; a2 < p->grid.ndim; ++a2) N *= p->grid.dims[a2];
+    const TexSet* ts = (p->dtype == SR_F32 && ctx->tex_enabled) ? texset_find(ctx, p->frames_dev, p->nframes, N) : nullptr;
+    ctx->job_use_tex = ts != nullptr;
+    for (int j = 0; j < p->k; ++j) nj.tex[j] = ts ? (unsigned long long)ts->tex[p->frame_index[j]] : 0ull;
+  }
   if (ctx->job_valid && std::memcmp(&nj, &ctx->job_last, sizeof(Job)) == 0) return SR_OK;
   // the previous upload may still be in flight from the pinned staging buffer
   CK(cudaStreamSynchronize(ctx->stream));
@@ -193,7 +227,7 @@ static int upload_job(sr_ctx* ctx, const sr_problem* p, const double* weights) {
 }
 
 static Launch launch_of(sr_ctx* ctx) {
-  return Launch{ctx->stream, ctx->sms, ctx->grid_override, ctx->legacy};
+  return Launch{ctx->stream, ctx->sms, ctx->grid_override, ctx->legacy, ctx->ws2};
 }
 
 #define SR_SWITCH(dtype, nd, FN, ...)                                    \
@@ -306,6 +340,10 @@ int sr_create(int32_t device, sr_ctx** out) {
     c->legacy = (lg && lg[0] == '1') ? 1 : 0;
     const char* db = getenv("SEQREG_B200_DEBUG");
     c->dbg = db ? atoi(db) : 0;
+    const char* w2 = getenv("SEQREG_B200_WS2");
+    c->ws2 = (w2 && w2[0] == '1') ? 1 : 0;
+    const char* tx = getenv("SEQREG_B200_TEX");
+    c->tex_enabled = (tx && tx[0] == '1') ? 1 : 0;
   }
   CK(cudaMalloc(&c->job_dev, sizeof(Job)));
   CK(cudaMalloc(&c->ticket, sizeof(unsigned)));
@@ -324,6 +362,7 @@ int sr_destroy(sr_ctx* c) {
   cudaFreeHost(c->job_host);
   cudaFree(c->part);
   cudaFree(c->ticket);
+  for (auto& t : c->texsets) texset_free(t);
   cudaFree(c->zbuf);
   cudaFree(c->aux);
   cudaFree(c->iaux);
@@ -341,6 +380,80 @@ int sr_set_grid_ctas(sr_ctx* c, int32_t ctas) {
   if (!c) return fail(SR_ERR_ARG, "null context");
   if (ctas < 0) return fail(SR_ERR_ARG, "ctas must be >= 0");
   c->grid_override = ctas;
+  return SR_OK;
+}
+
+int sr_frames_prepare(sr_ctx* c, int32_t dtype, const void* frames, int32_t nframes, const sr_grid* grid) {
+  if (!c || !frames || !grid || nframes < 1) return fail(SR_ERR_ARG, "bad sr_frames_prepare arguments");
+  int rc = check_grid(*grid);
+  if (rc) return rc;
+  if (dtype != SR_F32 || !c->tex_enabled) return SR_OK;  // fp64 frames (and the default) use global loads
+  const int n0 = grid->dims[0];
+  long long rows = 1;
+  for (int a = 1; a < grid->ndim; ++a) rows *= grid->dims[a];
+  if (n0 > 32768 || rows > 32768) return SR_OK;  // beyond the texture-gather limits: global loads
+  CK(cudaSetDevice(c->device));
+  for (auto it = c->texsets.begin(); it != c->texsets.end(); ++it)
+    if (it->ptr == frames) {
+      CK(cudaStreamSynchronize(c->stream));
+      texset_free(*it);
+      c->texsets.erase(it);
+      break;
+    }
+  TexSet t;
+  t.ptr = frames;
+  t.nframes = nframes;
+  t.N = (long long)n0 * rows;
+  const cudaChannelFormatDesc desc = cudaCreateChannelDesc<float>();
+  for (int f = 0; f < nframes; ++f) {
+    cudaArray_t arr = nullptr;
+    cudaError_t e = cudaMallocArray(&arr, &desc, n0, (size_t)rows, cudaArrayTextureGather);
+    if (e != cudaSuccess) {
+      texset_free(t);
+      return fail(SR_ERR_CUDA, "cudaMallocArray failed: %s", cudaGetErrorString(e));
+    }
+    t.arr.push_back(arr);
+    const float* src = reinterpret_cast<const float*>(frames) + (long long)f * t.N;
+    e = cudaMemcpy2DToArrayAsync(arr, 0, 0, src, (size_t)n0 * 4, (size_t)n0 * 4, (size_t)rows,
+                                 cudaMemcpyDeviceToDevice, c->stream);
+    if (e != cudaSuccess) {
+      texset_free(t);
+      return fail(SR_ERR_CUDA, "cudaMemcpy2DToArrayAsync failed: %s", cudaGetErrorString(e));
+    }
+    cudaResourceDesc res;
+    std::memset(&res, 0, sizeof res);
+    res.resType = cudaResourceTypeArray;
+    res.res.array.array = arr;
+    cudaTextureDesc td;
+    std::memset(&td, 0, sizeof td);
+    td.addressMode[0] = cudaAddressModeClamp;
+    td.addressMode[1] = cudaAddressModeClamp;
+    td.filterMode = cudaFilterModePoint;
+    td.readMode = cudaReadModeElementType;
+    td.normalizedCoords = 0;
+    cudaTextureObject_t tex = 0;
+    e = cudaCreateTextureObject(&tex, &res, &td, nullptr);
+    if (e != cudaSuccess) {
+      texset_free(t);
+      return fail(SR_ERR_CUDA, "cudaCreateTextureObject failed: %s", cudaGetErrorString(e));
+    }
+    t.tex.push_back(tex);
+  }
+  c->texsets.push_back(std::move(t));
+  c->job_valid = false;  // handles may have changed
+  return SR_OK;
+}
+
+int sr_frames_release(sr_ctx* c, const void* frames) {
+  if (!c) return fail(SR_ERR_ARG, "null context");
+  for (auto it = c->texsets.begin(); it != c->texsets.end(); ++it)
+    if (it->ptr == frames) {
+      CK(cudaStreamSynchronize(c->stream));
+      texset_free(*it);
+      c->texsets.erase(it);
+      c->job_valid = false;
+      break;
+    }
   return SR_OK;
 }
 

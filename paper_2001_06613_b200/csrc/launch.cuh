@@ -48,6 +48,7 @@ struct Launch {
   int sms;
   int grid_override;  // 0 = auto
   int legacy;         // 1 = force the non-specialized kernels (A/B checks)
+  int ws2;            // 1 = warp-specialized pass 2 (experimental)
 };
 
 template <typename K>
@@ -112,8 +113,30 @@ struct Runner {
     return cudaGetLastError();
   }
 
+  // warp-specialized pass 2 (NCC displacement, KP <= 32), engine_ws.cuh
+  static cudaError_t pass2_ws(const Launch& L, const Args& a, int* nblk_out) {
+    using C = WS2<T, KP>;
+    const size_t smem = ws2_smem<T, D, KP>();
+    auto kern = k_pass2_ws<T, D, KP>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const long long npix = a.pix_hi - a.pix_lo;
+    const long long ntiles = (npix + C::TP - 1) / C::TP;
+    int grid = occupancy_grid(L, kern, C::NT, smem, ntiles > 0 ? ntiles : 1);
+    Args b = a;
+    CUtensorMap ymap;
+    memset(&ymap, 0, sizeof ymap);
+    b.ymap_ok = encode_y_map<T>(&ymap, a, a.K * D, C::TP) ? 1 : 0;
+    kern<<<grid, C::NT, smem, L.stream>>>(b, ymap);
+    *nblk_out = grid;
+    return cudaGetLastError();
+  }
+
   static cudaError_t pass2(const Launch& L, const Args& a, double* part_aff, size_t aff_cap,
                            int* nblk_out) {
+    if constexpr (FEAT == NCC && PARAM == DISP && KP <= 32) {
+      if (!L.legacy && L.ws2) return pass2_ws(L, a, nblk_out);
+    }
     using C = G2<T, KP>;
     constexpr int NA = D * (D + 1);
     size_t smem = pass2_smem<T, D, FEAT, KP>();
