@@ -32,6 +32,11 @@ struct sr_ctx {
   int dbg = 0;     // SEQREG_B200_DEBUG: profiling experiment bits
   int ws2 = 0;     // SEQREG_B200_WS2=1: warp-specialized pass 2
   int tex_enabled = 0;  // SEQREG_B200_TEX=1: texture-gather sampling (measured slower on B200)
+  int tc = 1;      // SEQREG_B200_TC=0: SIMT Gram instead of tcgen05 in pass 1
+  int tc2 = 0;     // SEQREG_B200_TC2=1: tcgen05 pass 2
+  int split = 0;   // SEQREG_B200_SPLIT=1: split pass 1 (sampling kernel + tensor-core Gram kernel)
+  float* vbuf = nullptr;  // split pass 1: V = v - shift, [K][vstride]
+  size_t vbuf_bytes = 0;
   Job* job_dev = nullptr;
   Job* job_host = nullptr;  // pinned staging
   Job job_last{};           // content of the last upload (skip identical re-uploads)
@@ -227,7 +232,7 @@ static int upload_job(sr_ctx* ctx, const sr_problem* p, const double* weights) {
 }
 
 static Launch launch_of(sr_ctx* ctx) {
-  return Launch{ctx->stream, ctx->sms, ctx->grid_override, ctx->legacy, ctx->ws2};
+  return Launch{ctx->stream, ctx->sms, ctx->grid_override, ctx->legacy, ctx->ws2, ctx->tc, ctx->split, ctx->tc2};
 }
 
 #define SR_SWITCH(dtype, nd, FN, ...)                                    \
@@ -250,9 +255,17 @@ static cudaError_t launch_reduce_finalize(sr_ctx* c, const sr_problem* p, int nb
 
 // pass 1 over the slab, then the fixed-order cross-CTA reduction into raw (and, with
 // stats != nullptr, the finalize in the same launch)
+// KP of the pass-1 partial layout: the tcgen05 kernel always uses 32 (frames padded)
+static int pass1_kp(const sr_ctx* c, const sr_problem* p) {
+  if (p->dtype == SR_F32 && p->feature == SR_NCC && p->param == SR_DISPLACEMENT && p->k <= 32 && !c->legacy &&
+      c->tc)
+    return 32;
+  return kp_of(p->k);
+}
+
 static int corr_partial_impl(sr_ctx* c, const sr_problem* p, double* raw, double h = 0.0,
                              double* stats = nullptr) {
-  const int KP = kp_of(p->k);
+  const int KP = pass1_kp(c, p);
   const size_t stride = (size_t)KP * KP + 3 * KP;
   const size_t want = stride * (size_t)c->sms * 4;
   int rc = ensure_d(&c->part, &c->part_cap, want);
@@ -260,7 +273,18 @@ static int corr_partial_impl(sr_ctx* c, const sr_problem* p, double* raw, double
   Args a = make_args(c, p);
   const Launch L = launch_of(c);
   int nblk = 0;
-  CK(SR_SWITCH(p->dtype, p->grid.ndim, pass1, p->feature, p->param, KP, L, a, c->part, c->part_cap, &nblk));
+  const long long npix = p->pix_hi - p->pix_lo;
+  if (KP == 32 && p->dtype == SR_F32 && p->feature == SR_NCC && p->param == SR_DISPLACEMENT && c->split && npix > 0) {
+    const long long vstride = (npix + 3) & ~3LL;
+    void* vb = c->vbuf;
+    rc = ensure(&vb, &c->vbuf_bytes, (size_t)p->k * vstride * 4);
+    if (rc) return rc;
+    c->vbuf = (float*)vb;
+    if (p->grid.ndim == 2) CK(pass1_split_d2(L, a, c->vbuf, vstride, c->part, c->part_cap, &nblk));
+    else CK(pass1_split_d3(L, a, c->vbuf, vstride, c->part, c->part_cap, &nblk));
+  } else {
+    CK(SR_SWITCH(p->dtype, p->grid.ndim, pass1, p->feature, p->param, KP, L, a, c->part, c->part_cap, &nblk));
+  }
   const long long count = (long long)(p->pix_hi - p->pix_lo);
   const int fin = stats != nullptr;
   if (p->dtype == SR_F32)
@@ -344,6 +368,12 @@ int sr_create(int32_t device, sr_ctx** out) {
     c->ws2 = (w2 && w2[0] == '1') ? 1 : 0;
     const char* tx = getenv("SEQREG_B200_TEX");
     c->tex_enabled = (tx && tx[0] == '1') ? 1 : 0;
+    const char* tcs = getenv("SEQREG_B200_TC");
+    c->tc = (tcs && tcs[0] == '0') ? 0 : 1;
+    const char* sp = getenv("SEQREG_B200_SPLIT");
+    c->split = (sp && sp[0] == '1') ? 1 : 0;
+    const char* t2 = getenv("SEQREG_B200_TC2");
+    c->tc2 = (t2 && t2[0] == '1') ? 1 : 0;
   }
   CK(cudaMalloc(&c->job_dev, sizeof(Job)));
   CK(cudaMalloc(&c->ticket, sizeof(unsigned)));
@@ -362,6 +392,7 @@ int sr_destroy(sr_ctx* c) {
   cudaFreeHost(c->job_host);
   cudaFree(c->part);
   cudaFree(c->ticket);
+  cudaFree(c->vbuf);
   for (auto& t : c->texsets) texset_free(t);
   cudaFree(c->zbuf);
   cudaFree(c->aux);

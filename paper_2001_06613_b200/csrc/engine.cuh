@@ -1227,3 +1227,4 @@ __global__ void __launch_bounds__(256) k_frame_mean(const T* __restrict__ frames
 }  // namespace sr
 
 #include "engine_ws.cuh"
+#include "engine_tc.cuh"

@@ -2,4 +2,8 @@
 #include "launch.cuh"
 namespace sr {
 SR_DEFINE_INST(f32, float, 2)
+cudaError_t pass1_split_d2(const Launch& L, const Args& a, float* V, long long vstride, double* part, size_t cap,
+                           int* nblk) {
+  return run_pass1_split<2>(L, a, V, vstride, part, cap, nblk);
+}
 }  // namespace sr

@@ -71,6 +71,22 @@ def main():
         eng.set_grid_ctas(ctas)
         res[f"pass1 ctas={ctas}"] = timeit(lambda: plan.corr_partial(prob), flush, args.reps)
     eng.set_grid_ctas(0)
+
+    class NoFlush:
+        def fill_(self, v):
+            pass
+
+    res["pass1 warm L2 (no flush)"] = timeit(lambda: plan.corr_partial(prob), NoFlush(), args.reps)
+    res["pass2 warm L2 (no flush)"] = timeit(lambda: plan.grad(prob, g), NoFlush(), args.reps)
+    fr_only = fd.data
+
+    class FramesHot:  # flush, then pull the frames (33.5 MB) back into L2
+        def fill_(self, v):
+            flush.fill_(v)
+            fr_only.sum()
+
+    res["pass1 frames in L2, y cold"] = timeit(lambda: plan.corr_partial(prob), FramesHot(), args.reps)
+    res["pass2 frames in L2, y cold"] = timeit(lambda: plan.grad(prob, g), FramesHot(), args.reps)
     prob_pad = plan.problem(y=ypad)
     res["pass1 y-stride N+1 (no TMA/vec)"] = timeit(lambda: plan.corr_partial(prob_pad), flush, args.reps)
     prob = plan.problem(y=y)

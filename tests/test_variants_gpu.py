@@ -1,0 +1,73 @@
+"""Every kernel variant selectable by environment switch (read once per engine context) gives the
+oracle's D and dD/dy: each variant runs the fp32 field parity cases in a fresh process.
+
+    SEQREG_B200_LEGACY=1  non-specialized pass 1 / pass 2
+    SEQREG_B200_TC=0      warp-specialized SIMT Gram in pass 1 (no tcgen05)
+    SEQREG_B200_TC2=1     tcgen05 pass 2 (2-D)
+    SEQREG_B200_SPLIT=1   split pass 1: sampling kernel + tcgen05 Gram kernel
+    SEQREG_B200_WS2=1     warp-specialized SIMT pass 2
+"""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CHILD = r"""
+import json, sys
+import numpy as np, torch
+import paper_2001_06613_b200 as srb
+from oracle import seqreg_oracle as orc
+from scipy.ndimage import gaussian_filter
+
+out = []
+for dims, K, seed in [((64, 48), 32, 1), ((40, 36), 20, 2), ((200, 150), 32, 3), ((12, 11, 10), 32, 4)]:
+    rng = np.random.default_rng(seed)
+    d = len(dims)
+    sp = tuple([0.5, 0.25, 0.75][:d])
+    org = tuple(-n * s / 2 for n, s in zip(dims, sp))
+    frames = np.stack([gaussian_filter(rng.standard_normal(dims), 1.5, mode="reflect").ravel(order="F") + 3.0
+                       for _ in range(K)])
+    x = orc.cell_centers(dims, sp, org).T
+    y = x[None] + 0.4 * rng.standard_normal((K,) + x.shape) * np.asarray(sp)[None, :, None]
+    # keep samples off grid nodes, where the interpolant's derivative jumps and an fp32 rounding of y
+    # flips the cell (the kink hazard; covered separately by the dyadic identity test)
+    s_ = np.asarray(sp)[None, :, None]
+    o_ = np.asarray(org)[None, :, None]
+    t_ = (y - o_) / s_ - 0.5
+    fr = t_ - np.floor(t_)
+    y = np.where((fr < 2e-3) | (fr > 1 - 2e-3), y + 5e-3 * s_, y)
+    w = rng.uniform(0.5, 1.0, K)
+    h = float(np.prod(sp))
+    fd = srb.DeviceFrames.from_array(srb.get_engine(), frames, srb.GridSpec(dims, sp, org), torch.float32)
+    obj = srb.FieldObjective(fd, list(range(K)), w, h)
+    yt = torch.as_tensor(y).to(device=fd.data.device, dtype=torch.float32).contiguous()
+    stats, g = obj.evaluate(yt)
+    D = float(stats[0].item())
+    q = frames.astype(np.float32).astype(np.float64)
+    yq = y.astype(np.float32).astype(np.float64)
+    _, Dref, gref = orc.evaluate_field(list(q), dims, sp, org, yq, w, h)
+    gd = g.double().cpu().numpy()
+    out.append({"dims": list(dims), "K": K, "dD": abs(D - Dref) / abs(Dref),
+                "dg": float(np.abs(gd - gref).max() / np.abs(gref).max())})
+print(json.dumps(out))
+"""
+
+
+@pytest.mark.parametrize("env", ["SEQREG_B200_LEGACY=1", "SEQREG_B200_TC=0", "SEQREG_B200_TC2=1",
+                                 "SEQREG_B200_SPLIT=1", "SEQREG_B200_WS2=1", ""])
+def test_variant_parity(env):
+    e = dict(os.environ)
+    if env:
+        k, v = env.split("=")
+        e[k] = v
+    r = subprocess.run([sys.executable, "-c", CHILD], cwd=ROOT, env=e, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    for case in json.loads(r.stdout.strip().splitlines()[-1]):
+        assert case["dD"] < 1e-4 and case["dg"] < 1e-4, (env, case)
