@@ -34,7 +34,7 @@ struct sr_ctx {
   int tex_enabled = 0;  // SEQREG_B200_TEX=1: texture-gather sampling (measured slower on B200)
   int tc = 1;      // SEQREG_B200_TC=0: SIMT Gram instead of tcgen05 in pass 1
   int tc2 = 0;     // SEQREG_B200_TC2=1: tcgen05 pass 2
-  int split = 0;   // SEQREG_B200_SPLIT=1: split pass 1 (sampling kernel + tensor-core Gram kernel)
+  int split = 1;   // SEQREG_B200_SPLIT=0: fused tensor-core pass 1 instead of sampling kernel + Gram kernel
   float* vbuf = nullptr;  // split pass 1: V = v - shift, [K][vstride]
   size_t vbuf_bytes = 0;
   Job* job_dev = nullptr;
@@ -274,8 +274,9 @@ static int corr_partial_impl(sr_ctx* c, const sr_problem* p, double* raw, double
   const Launch L = launch_of(c);
   int nblk = 0;
   const long long npix = p->pix_hi - p->pix_lo;
-  if (KP == 32 && p->dtype == SR_F32 && p->feature == SR_NCC && p->param == SR_DISPLACEMENT && c->split && npix > 0) {
-    const long long vstride = (npix + 3) & ~3LL;
+  if (KP == 32 && p->dtype == SR_F32 && p->feature == SR_NCC && p->param == SR_DISPLACEMENT && c->split && c->tc &&
+      !c->legacy && npix > 0) {
+    const long long vstride = (npix + 3) & ~3LL;  // V = v - shift, [K][vstride]
     void* vb = c->vbuf;
     rc = ensure(&vb, &c->vbuf_bytes, (size_t)p->k * vstride * 4);
     if (rc) return rc;
@@ -371,7 +372,7 @@ int sr_create(int32_t device, sr_ctx** out) {
     const char* tcs = getenv("SEQREG_B200_TC");
     c->tc = (tcs && tcs[0] == '0') ? 0 : 1;
     const char* sp = getenv("SEQREG_B200_SPLIT");
-    c->split = (sp && sp[0] == '1') ? 1 : 0;
+    c->split = (sp && sp[0] == '0') ? 0 : 1;
     const char* t2 = getenv("SEQREG_B200_TC2");
     c->tc2 = (t2 && t2[0] == '1') ? 1 : 0;
   }

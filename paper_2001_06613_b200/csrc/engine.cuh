@@ -604,67 +604,61 @@ __device__ void finalize_block(const double* __restrict__ raw, const Job* job, i
     Cmat[j * K + i] = c;
   }
   __syncthreads();
-  // D = h * [(sum w)^2 - sum w^2 - sum_{i != j} w_i w_j C_ij^2]   (similarity.py:167-177)
-  double part = 0.0;
-  for (int e = tid; e < K * K; e += nt) {
-    const int i = e / K, j = e % K;
-    const double c = Cmat[e];
-    stats[L.C + e] = c;
-    if (i != j) part += w[i] * w[j] * c * c;
-  }
-  red[tid] = part;
-  // c_j = sum_i w_i C_ij^2  (= f_j . g_j, similarity.py:210)
-  if (tid < K) {
-    double c = 0.0;
-    for (int i = 0; i < K; ++i) {
-      const double v = Cmat[i * K + tid];
-      c += w[i] * v * v;
+  // warp per column j, lanes over i, fixed-order shuffle reductions:
+  //   c_j = sum_i w_i C_ij^2  (= f_j . g_j, similarity.py:210)
+  //   dcol_j = sum_{i != j} w_i w_j C_ij^2  (D = h [(sum w)^2 - sum w^2 - sum_j dcol_j], similarity.py:167-177)
+  const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  for (int j = warp; j < K; j += nw) {
+    double cp = 0.0, dp = 0.0;
+    for (int i = lane; i < K; i += 32) {
+      const double c = Cmat[i * K + j];
+      stats[L.C + i * K + j] = c;
+      const double wc2 = w[i] * c * c;
+      cp += wc2;
+      if (i != j) dp += wc2 * w[j];
     }
-    cj[tid] = c;
+    cp = warp_sum(cp);
+    dp = warp_sum(dp);
+    if (lane == 0) {
+      cj[j] = cp;
+      red[j] = dp;
+    }
   }
   __syncthreads();
-  for (int o = nt / 2; o > 0; o >>= 1) {
-    if (tid < o) red[tid] += red[tid + o];
-    __syncthreads();
+  // M'_ij = -4 h w_j (w_i C_ij / sig_i - delta_ij c_j / sig_j) / sig_j ;  beta'_j = -sum_i M'_ij mu_i
+  float* Mf = reinterpret_cast<float*>(stats + L.Mf);
+  for (int j = warp; j < K; j += nw) {
+    double bp = 0.0;
+    for (int i = lane; i < K; i += 32) {
+      double m = 0.0;
+      if (!deg[i] && !deg[j]) {
+        double t = w[i] * Cmat[i * K + j] * isg[i];
+        if (i == j) t -= cj[j] * isg[j];
+        m = -4.0 * h * w[j] * t * isg[j];
+      }
+      stats[L.M + i * K + j] = m;
+      Mf[i * K + j] = (float)m;
+      bp += m * mu[i];
+    }
+    bp = warp_sum(bp);
+    if (lane == 0) stats[L.beta + j] = feat == NCC ? -bp : 0.0;
   }
-  if (tid == 0) {
-    double sw = 0.0, sw2 = 0.0;
-    for (int i = 0; i < K; ++i) {
+  if (warp == 0) {
+    double dsum = 0.0, sw = 0.0, sw2 = 0.0;
+    for (int i = lane; i < K; i += 32) {
+      dsum += red[i];
       sw += w[i];
       sw2 += w[i] * w[i];
     }
-    const double pair_mass = sw * sw - sw2;
-    stats[0] = fmax(0.0, h * (pair_mass - red[0]));
-    stats[1] = K;
-    stats[2] = N;
-    stats[3] = h;
-  }
-  // M'_ij = -4 h w_j (w_i C_ij / sig_i - delta_ij c_j / sig_j) / sig_j ;  beta'_j = -sum_i M'_ij mu_i
-  float* Mf = reinterpret_cast<float*>(stats + L.Mf);
-  for (int e = tid; e < K * K; e += nt) {
-    const int i = e / K, j = e % K;
-    double m = 0.0;
-    if (!deg[i] && !deg[j]) {
-      double t = w[i] * Cmat[e] * isg[i];
-      if (i == j) t -= cj[j] * isg[j];
-      m = -4.0 * h * w[j] * t * isg[j];
+    dsum = warp_sum(dsum);
+    sw = warp_sum(sw);
+    sw2 = warp_sum(sw2);
+    if (lane == 0) {
+      stats[0] = fmax(0.0, h * ((sw * sw - sw2) - dsum));
+      stats[1] = K;
+      stats[2] = N;
+      stats[3] = h;
     }
-    stats[L.M + e] = m;
-    Mf[e] = (float)m;
-  }
-  if (tid < K) {
-    const int j = tid;
-    double b = 0.0;
-    if (feat == NCC && !deg[j]) {
-      const double aj = -4.0 * h * w[j] * isg[j];
-      for (int i = 0; i < K; ++i) {
-        if (deg[i]) continue;
-        double t = w[i] * Cmat[i * K + j] * isg[i];
-        if (i == j) t -= cj[j] * isg[j];
-        b -= aj * t * mu[i];
-      }
-    }
-    stats[L.beta + j] = b;
   }
 }
 

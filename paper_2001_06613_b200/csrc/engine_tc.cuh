@@ -267,109 +267,124 @@ namespace sr {
 // Thread = 4 pixels (lane-consecutive, stride 256) of one subset frame; writes the shifted
 // value v - shift to V[k][p - pix_lo] (row stride vstride).  Read y (d floats) + gather T,
 // write V: the sampling runs at full occupancy with no Gram registers or barriers.
-template <int D, bool POW2>
-__device__ __forceinline__ void sample_v_body(const Args& a, float* __restrict__ V, long long vstride) {
-  // 32-bit offsets inside a plane; 64-bit arithmetic only for the per-block plane pointers
+template <int D, bool POW2, int SPT>
+__global__ void __launch_bounds__(256, 8) k_sample_v(const Args a, float* __restrict__ V, long long vstride) {
+  // grid (pixel blocks, K): block-uniform 64-bit bases, 32-bit per-thread offsets
+  constexpr int BP = 256 * SPT;  // pixels per block
   const int npix = (int)(a.pix_hi - a.pix_lo);
-  const int per_frame = (npix + 1023) >> 10;
-  const int k = (int)blockIdx.x / per_frame;
-  const int p0 = ((int)blockIdx.x - k * per_frame) * 1024 + (int)threadIdx.x;
+  const int k = (int)blockIdx.y;
+  const int b0 = (int)blockIdx.x * BP;
+  const int tid = (int)threadIdx.x;
   const int fi = a.job->frame_index[k];
   const float* img = reinterpret_cast<const float*>(a.frames) + (long long)fi * a.g.N;
-  const float* shifts = reinterpret_cast<const float*>(a.shifts);
-  const float sh = shifts ? shifts[fi] : 0.f;
-  const float* yp[D];
+  const float* yb = reinterpret_cast<const float*>(a.y) + (long long)(k * D) * a.y_stride + (a.pix_lo - a.y_off) + b0;
+  float* vb = V + (long long)k * vstride + b0;
+  const int nb = npix - b0;  // pixels left from this block's start
+  const bool full = nb >= BP;
+  float p[SPT][D];
 #pragma unroll
-  for (int c = 0; c < D; ++c)
-    yp[c] = reinterpret_cast<const float*>(a.y) + (long long)(k * D + c) * a.y_stride + (a.pix_lo - a.y_off);
-  float* row = V + (long long)k * vstride;
-  float p[4][D];
+  for (int e = 0; e < SPT; ++e) {
+    const int pe = full ? tid + 256 * e : min(tid + 256 * e, nb - 1);
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    const int pe = min(p0 + 256 * e, npix - 1);
-#pragma unroll
-    for (int c = 0; c < D; ++c) p[e][c] = __ldg(yp[c] + pe);
+    for (int c = 0; c < D; ++c) p[e][c] = __ldg(yb + (long long)c * a.y_stride + pe);
   }
-  float v[4];
+  float v[SPT];
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
+  for (int e = 0; e < SPT; ++e) {
     float gd[D];
     v[e] = interp<float, float, D, false, POW2>(img, a.g, p[e], gd);
   }
+  const float* shifts = reinterpret_cast<const float*>(a.shifts);
+  const float sh = shifts ? shifts[fi] : 0.f;
+  if (full) {
 #pragma unroll
-  for (int e = 0; e < 4; ++e)
-    if (p0 + 256 * e < npix) row[p0 + 256 * e] = v[e] - sh;
+    for (int e = 0; e < SPT; ++e) vb[tid + 256 * e] = v[e] - sh;
+  } else {
+#pragma unroll
+    for (int e = 0; e < SPT; ++e)
+      if (tid + 256 * e < nb) vb[tid + 256 * e] = v[e] - sh;
+  }
 }
 
-template <int D>
-__global__ void __launch_bounds__(256) k_sample_v(const Args a, float* __restrict__ V, long long vstride) {
-  if (a.g.pow2) sample_v_body<D, true>(a, V, vstride);
-  else sample_v_body<D, false>(a, V, vstride);
-}
-
-// Split pass 1, kernel B: the K x K raw Gram of V on the tensor cores.  A TMA box of
-// [32 frames x 128 pixels] (zero-filled past K and past the slab) lands in a plain stage; 4
-// splitter warps turn it into the hi/lo SW128 operand tile and keep per-frame sum / max / min;
-// one thread issues the tcgen05 MMAs; 4 consumer warps flush the ping-pong TMEM accumulators
-// into fp64.  Output: the same per-CTA partial layout as pass 1 ([32*32 | s | max | -min]).
+// Split pass 1, kernel B: the K x K raw Gram of V on the tensor cores.  mbarrier pipeline,
+// no CTA-wide barrier inside the loop:
+//   issuer lane (warp 16): TMA box [32 frames x 128 pixels] of V -> stage (zero-filled past K
+//     and past the slab); per tile 16 MMAs (M64 N32 K8, A = [V_hi; V_lo], B = V_hi) into TMEM
+//     accumulator ring slot n % NA; tcgen05.commit frees the operand buffer and fills the slot;
+//   16 splitter warps: stage -> hi/lo SW128 operand buffer n % NB, per-frame sum / max / min;
+//   4 flusher warps: TMEM slot -> fp64 accumulators in smem (G = HH + LH + LH^T at the end).
+// The flush lags the MMAs by up to NA tiles, so it never stalls the splitters.
 struct TCG {
-  static constexpr int NS_ = 512, NC = 128, NT = NS_ + NC;  // splitters + consumers
-  static constexpr int KP = 32, TP = 128, NST = 3;
+  static constexpr int NSP = 512, NT = NSP + 32 + 128;  // splitters, issuer warp, flushers
+  static constexpr int KP = 32, TP = 128, NST = 6, NB = 3, NA = 4, NACC = 4;  // NACC chains per tile
   static constexpr int VBYTES = 64 * TP * 4, SBYTES = KP * TP * 4;
-  static constexpr int BAR_FULL = 1, BAR_EMPTY = 3, BAR_SPLIT = 5, BAR_CONS = 6;
   static constexpr uint32_t IDESC = umma_idesc_tf32(64, 32);
 };
 
 constexpr size_t tcg_smem() {
-  return 1024 + (size_t)TCG::NST * TCG::SBYTES + 2 * (size_t)TCG::VBYTES + 128 + 64 * 33 * 8;
+  return 1024 + (size_t)TCG::NST * TCG::SBYTES + (size_t)TCG::NB * TCG::VBYTES + 256 + 64 * 33 * 8;
 }
 
-static __global__ void __launch_bounds__(TCG::NT, 1) k_gram_tc(const Args a, const __grid_constant__ CUtensorMap vmap,
-                                                        long long vcols) {
+static __global__ void __launch_bounds__(TCG::NT, 1) k_gram_tc(const Args a, const __grid_constant__ CUtensorMap vmap) {
   using C = TCG;
-  constexpr int TP = C::TP, NT = C::NT, NC = C::NC, KP = C::KP, NST = C::NST;
+  constexpr int TP = C::TP, KP = C::KP, NST = C::NST, NB = C::NB, NA = C::NA;
   extern __shared__ __align__(1024) unsigned char smem_tcg[];
   unsigned char* base = smem_tcg + ((1024 - (smem_u32(smem_tcg) & 1023)) & 1023);
-  float* stage = reinterpret_cast<float*>(base);                                // [NST][32][TP]
-  unsigned char* Vb = base + (size_t)NST * C::SBYTES;                           // [2][VBYTES]
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(Vb + 2 * (size_t)C::VBYTES);     // [NST] + [2]
-  uint64_t* mbar_mma = mbar + NST;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar_mma + 2);
-  double* accs = reinterpret_cast<double*>(mbar + 16);
+  float* stage = reinterpret_cast<float*>(base);                             // [NST][32][TP]
+  unsigned char* Vb = base + (size_t)NST * C::SBYTES;                        // [NB][VBYTES]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(Vb + (size_t)NB * C::VBYTES);
+  uint64_t* st_full = bars;              // [NST] TMA transaction barriers
+  uint64_t* vb_full = st_full + NST;     // [NB]  512 splitter arrivals
+  uint64_t* vb_free = vb_full + NB;      // [NB]  tcgen05.commit
+  uint64_t* acc_full = vb_free + NB;     // [NA]  tcgen05.commit
+  uint64_t* acc_free = acc_full + NA;    // [NA]  128 flusher arrivals
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_free + NA);
+  double* accs = reinterpret_cast<double*>(bars + 32);                       // [64][33]
 
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int K = a.K;
   const long long npix = a.pix_hi - a.pix_lo;
   const long long ntiles = (npix + TP - 1) / TP;
-  const long long nloc = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  auto issue = [&](long long n) {
-    if (n >= nloc) return;
-    const long long c0 = (blockIdx.x + n * gridDim.x) * TP;  // column of V (pixel - pix_lo)
-    const int s = (int)(n % NST);
-    mbar_arrive_expect_tx(&mbar[s], (uint32_t)C::SBYTES);
-    tma_load_2d(stage + (size_t)s * KP * TP, &vmap, (int)c0, 0, &mbar[s]);
-  };
+  const long long nloc = (a.dbg & 256) ? 0 : ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   if (tid == 0) {
-    for (int s = 0; s < NST; ++s) mbar_init(&mbar[s], 1);
-    mbar_init(&mbar_mma[0], 1);
-    mbar_init(&mbar_mma[1], 1);
+    for (int s = 0; s < NST; ++s) mbar_init(&st_full[s], 1);
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(&vb_full[b], C::NSP);
+      mbar_init(&vb_free[b], 1);
+    }
+    for (int s = 0; s < NA; ++s) {
+      mbar_init(&acc_full[s], 1);
+      mbar_init(&acc_free[s], 128);
+    }
     fence_mbar_init();
     tma_prefetch_desc(&vmap);
   }
-  for (int e = tid; e < 2 * C::VBYTES / 4; e += NT) reinterpret_cast<float*>(Vb)[e] = 0.f;
-  if (tid >= C::NS_ && tid < C::NS_ + 32) tmem_alloc(tmem_slot, 64);
+  if (K < KP) {  // operand rows K..31 (hi) and 32+K..63 (lo) stay zero; rows < K are rewritten every tile
+    const int zr = KP - K;
+    for (int e = tid; e < NB * 2 * zr * 128; e += C::NT) {
+      const int b = e / (2 * zr * 128), rr = (e / 128) % (2 * zr), w = e % 128;
+      const int row = rr < zr ? K + rr : 32 + K + (rr - zr);
+      // word w % 32 of the 128-byte row in column atom w / 32 (a whole row: the swizzle is irrelevant)
+      *reinterpret_cast<float*>(Vb + (size_t)b * C::VBYTES + (w >> 5) * 8192 + (row >> 3) * 1024 + (row & 7) * 128 +
+                                (w & 31) * 4) = 0.f;
+    }
+  }
+  for (int e = tid; e < 64 * 33; e += C::NT) accs[e] = 0.0;
+  if (warp == C::NSP / 32) tmem_alloc(tmem_slot, 32 * NA * C::NACC);
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   double* out = a.part + (size_t)blockIdx.x * (KP * KP + 3 * KP);
-  (void)vcols;
+  auto tile_col = [&](long long n) { return (blockIdx.x + n * gridDim.x) * TP; };
+  auto load_tile = [&](long long n, int st) {  // box [32 frames x 128 pixels], zero-filled past K / the slab
+    mbar_arrive_expect_tx(&st_full[st], (uint32_t)C::SBYTES);
+    tma_load_2d(stage + (size_t)st * KP * TP, &vmap, (int)tile_col(n), 0, &st_full[st]);
+  };
 
-  if (tid < C::NS_) {
+  if (tid < C::NSP) {
     // =============================== splitters: frame row r = tid / 16, two float4 groups each
-    if (tid == 0)
-      for (int s = 0; s < NST; ++s) issue(s);
     const int r = tid >> 4, part = tid & 15;
     // group g (of 32 per 128-pixel row) = 2 part + h; atom g / 8 (8 KB column block), chunk g % 8
     uint32_t off_hi[2], off_lo[2];
@@ -382,17 +397,19 @@ static __global__ void __launch_bounds__(TCG::NT, 1) k_gram_tc(const Args a, con
     }
     float fsum = 0.f, fmx = -INFINITY, fmn = INFINITY;
     for (long long n = 0; n < nloc; ++n) {
-      const int b = (int)(n & 1), st = (int)(n % NST);
-      const long long rem = npix - (blockIdx.x + n * gridDim.x) * TP;
-      mbar_wait(&mbar[st], (uint32_t)((n / NST) & 1));
-      named_sync(C::BAR_EMPTY + b, NT);
+      const int b = (int)(n % NB), st = (int)(n % NST);
+      const long long rem = npix - tile_col(n);
+      mbar_wait(&st_full[st], (uint32_t)((n / NST) & 1));
+      float4 q4[2];
       const float* src = stage + (size_t)st * KP * TP + (size_t)r * TP + part * 8;
+      q4[0] = *reinterpret_cast<const float4*>(src);
+      q4[1] = *reinterpret_cast<const float4*>(src + 4);
+      if (n >= NB) mbar_wait(&vb_free[b], (uint32_t)((n / NB - 1) & 1));
       unsigned char* vb = Vb + (size_t)b * C::VBYTES;
-      if (r < K) {
+      if (r < K && !(a.dbg & 128)) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const float4 q4 = *reinterpret_cast<const float4*>(src + 4 * h);
-          const float qv[4] = {q4.x, q4.y, q4.z, q4.w};
+          const float qv[4] = {q4[h].x, q4[h].y, q4[h].z, q4[h].w};
           float hi[4], lo[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
@@ -409,9 +426,7 @@ static __global__ void __launch_bounds__(TCG::NT, 1) k_gram_tc(const Args a, con
         }
       }
       fence_proxy_async_smem();
-      named_sync(C::BAR_SPLIT, C::NS_);  // stage st fully consumed
-      named_arrive(C::BAR_FULL + b, NT);
-      if (tid == 0) issue(n + NST);
+      mbar_arrive(&vb_full[b]);  // also releases stage st (read above)
     }
     // per-frame sums over the 16 threads of a row (fixed xor tree); extrema of v - shift
     double s = (double)fsum;
@@ -428,56 +443,63 @@ static __global__ void __launch_bounds__(TCG::NT, 1) k_gram_tc(const Args a, con
       out[KP * KP + KP + r] = (double)fmx + sh;      // max v  (= max(v - shift) + shift)
       out[KP * KP + 2 * KP + r] = -((double)fmn + sh);
     }
-  } else {
-    // =============================== consumers (as in k_pass1_tc)
-    const int ct = tid - C::NS_, cw = ct >> 5, cl = ct & 31;
-    const int mrow = 16 * cw + cl;
-    if (cl < 16)
-      for (int c = 0; c < 32; ++c) accs[mrow * 33 + c] = 0.0;
-    auto flush = [&](long long m) {
-      const int bm = (int)(m & 1);
-      mbar_wait(&mbar_mma[bm], (uint32_t)((m >> 1) & 1));
-      tc_fence_after();
-      float v[32];
-      tmem_ld32(tmem + ((uint32_t)(cw * 32) << 16) + (uint32_t)(bm * 32), v);
-      if (cl < 16) {
-#pragma unroll
-        for (int c = 0; c < 32; ++c) accs[mrow * 33 + c] += (double)v[c];
-      }
-      tc_fence_before();
-      if (m + 2 < nloc) named_arrive(C::BAR_EMPTY + bm, NT);
-    };
-    if (nloc > 0) named_arrive(C::BAR_EMPTY + 0, NT);
-    if (nloc > 1) named_arrive(C::BAR_EMPTY + 1, NT);
-    for (long long n = 0; n < nloc; ++n) {
-      const int b = (int)(n & 1);
-      named_sync(C::BAR_FULL + b, NT);
-      named_sync(C::BAR_CONS, NC);
-      if (ct == 0) {
+  } else if (warp == C::NSP / 32) {
+    // =============================== issuer: TMA loads and MMAs
+    if (lane == 0) {
+      for (long long n = 0; n < nloc && n < NST; ++n) load_tile(n, (int)n);
+      for (long long n = 0; n < nloc; ++n) {
+        const int b = (int)(n % NB), s = (int)(n % NA), st = (int)(n % NST);
+        mbar_wait(&vb_full[b], (uint32_t)((n / NB) & 1));
+        if (n + NST < nloc) load_tile(n + NST, st);  // every splitter has read stage st: refill it
+        if (n >= NA) mbar_wait(&acc_free[s], (uint32_t)((n / NA - 1) & 1));
         tc_fence_after();
         const uint32_t vaddr = smem_u32(Vb + (size_t)b * C::VBYTES);
 #pragma unroll
-        for (int s = 0; s < TP / 8; ++s) {
-          const uint64_t d = umma_sdesc_sw128(vaddr + (uint32_t)((s >> 2) * 8192 + (s & 3) * 32));
-          umma_tf32(tmem + (uint32_t)(b * 32), d, d, C::IDESC, s > 0 ? 1u : 0u);
+        for (int k8 = 0; k8 < TP / 8; ++k8) {
+          if (a.dbg & 64) break;
+          const uint64_t d = umma_sdesc_sw128(vaddr + (uint32_t)((k8 >> 2) * 8192 + (k8 & 3) * 32));
+          umma_tf32(tmem + (uint32_t)((s * C::NACC + k8 % C::NACC) * 32), d, d, C::IDESC,
+                    k8 >= C::NACC ? 1u : 0u);
         }
-        umma_commit(&mbar_mma[b]);
+        umma_commit(&vb_free[b]);
+        umma_commit(&acc_full[s]);
       }
-      __syncwarp();
-      if (n > 0) flush(n - 1);
     }
-    if (nloc > 0) flush(nloc - 1);
-    named_sync(C::BAR_CONS, NC);
-    for (int e = ct; e < KP * KP; e += NC) {
+    __syncwarp();
+  } else {
+    // =============================== flushers: TMEM lane quarter q = warp % 4 holds rows 16q..16q+15
+    const int q = warp & 3, mrow = 16 * q + lane;
+    double* acc = accs + mrow * 33;
+    for (long long n = 0; n < nloc; ++n) {
+      const int s = (int)(n % NA);
+      mbar_wait(&acc_full[s], (uint32_t)((n / NA) & 1));
+      tc_fence_after();
+      float v[32], w[32];
+      const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(s * C::NACC * 32);
+      tmem_ld32(ta, v);
+#pragma unroll
+      for (int c2 = 1; c2 < C::NACC; ++c2) {
+        tmem_ld32(ta + 32 * c2, w);
+#pragma unroll
+        for (int c = 0; c < 32; ++c) v[c] += w[c];
+      }
+      tc_fence_before();
+      mbar_arrive(&acc_free[s]);
+      if (lane < 16)
+#pragma unroll
+        for (int c = 0; c < 32; ++c) acc[c] += (double)v[c];
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (tid >= C::NSP + 32) {
+    for (int e = tid - (C::NSP + 32); e < KP * KP; e += 128) {
       const int i = e / KP, j = e % KP;
       out[e] = accs[i * 33 + j] + accs[(32 + i) * 33 + j] + accs[(32 + j) * 33 + i];
     }
-    tc_fence_before();
-    named_sync(C::BAR_CONS, NC);
-    if (cw == 0) {
-      tc_fence_after();
-      tmem_dealloc(tmem, 64);
-    }
+  } else if (warp == C::NSP / 32) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 32 * NA * C::NACC);
   }
 }
 

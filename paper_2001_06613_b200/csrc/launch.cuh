@@ -50,7 +50,7 @@ struct Launch {
   int legacy;         // 1 = force the non-specialized kernels (A/B checks)
   int ws2;            // 1 = warp-specialized pass 2 (experimental)
   int tc;             // 1 = tcgen05 Gram in pass 1 (fp32 NCC displacement, K <= 32)
-  int split;          // 1 = split pass 1 (sampling kernel + tensor-core Gram kernel)
+  int split;          // 1 = split pass 1 (sampling kernel + tensor-core Gram kernel; default)
   int tc2;            // 1 = tcgen05 pass 2 (2-D fp32 NCC displacement; slower than the SIMT pass 2 today)
 };
 
@@ -246,8 +246,11 @@ cudaError_t run_pass1_split(const Launch& L, const Args& a, float* V, long long 
                             size_t part_cap, int* nblk) {
   const long long npix = a.pix_hi - a.pix_lo;
   if (npix <= 0) return cudaErrorInvalidValue;
-  const long long per_frame = (npix + 1023) / 1024;
-  k_sample_v<D><<<(unsigned)(per_frame * a.K), 256, 0, L.stream>>>(a, V, vstride);
+  constexpr int SPT = 4;
+  const long long per_frame = (npix + 256 * SPT - 1) / (256 * SPT);
+  const dim3 sgrid((unsigned)per_frame, (unsigned)a.K);
+  if (a.g.pow2) k_sample_v<D, true, SPT><<<sgrid, 256, 0, L.stream>>>(a, V, vstride);
+  else k_sample_v<D, false, SPT><<<sgrid, 256, 0, L.stream>>>(a, V, vstride);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   EncodeTiledFn fn = encode_tiled_fn();
@@ -272,7 +275,7 @@ cudaError_t run_pass1_split(const Launch& L, const Args& a, float* V, long long 
   if ((size_t)grid * stride > part_cap) grid = (int)(part_cap / stride);
   Args b = a;
   b.part = part;
-  k_gram_tc<<<grid, TCG::NT, smem, L.stream>>>(b, vmap, npix);
+  k_gram_tc<<<grid, TCG::NT, smem, L.stream>>>(b, vmap);
   *nblk = grid;
   return cudaGetLastError();
 }

@@ -2,6 +2,8 @@
 vectors and the oracle.  Tolerances (north_star): 1e-10 relative in fp64, 1e-4 in fp32.
 Relative gradient errors are measured against the largest gradient entry."""
 
+import zlib
+
 import numpy as np
 import pytest
 import torch
@@ -135,6 +137,12 @@ def _random_problem(rng, dims, K, amp=0.4, nframes=None):
                        for _ in range(nframes)])
     x = orc.cell_centers(dims, spacing, origin).T
     y = x[None] + amp * rng.standard_normal((K,) + x.shape) * np.asarray(spacing)[None, :, None]
+    # keep samples off grid nodes: there the interpolant's derivative jumps, and an fp32 rounding of y
+    # can flip the cell (the kink hazard, pinned separately by test_identity_kink_gradient_fp32_dyadic)
+    s_, o_ = np.asarray(spacing)[None, :, None], np.asarray(origin)[None, :, None]
+    t_ = (y - o_) / s_ - 0.5
+    fr = t_ - np.floor(t_)
+    y = np.where((fr < 2e-3) | (fr > 1 - 2e-3), y + 5e-3 * s_, y)
     w = rng.uniform(0.5, 1.0, K)
     return frames, spacing, origin, y, w
 
@@ -145,7 +153,7 @@ def _random_problem(rng, dims, K, amp=0.4, nframes=None):
                                     ((12, 10), 100), ((10, 9, 8), 5), ((9, 8, 7), 20)])
 def test_field_parity_vs_oracle(feature, dtype, dims, K):
     """Displacement-field D and dD/dy vs the oracle, every KP bucket, 2-D and 3-D."""
-    rng = np.random.default_rng(hash((feature, str(dtype), dims, K)) % 2**32)
+    rng = np.random.default_rng(zlib.crc32(repr((feature, str(dtype), dims, K)).encode()))
     frames, spacing, origin, y, w = _random_problem(rng, dims, K, nframes=K + 2)
     subset0 = sorted(rng.choice(K + 2, size=K, replace=False).tolist())
     h = float(np.prod(spacing))
