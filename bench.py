@@ -183,7 +183,7 @@ def run_gpu(args):
         flush.fill_(1.0)
         step()
     torch.cuda.synchronize()
-    launches_per_step = obj.launches_per_step()
+    launches_per_step = count_engine_launches(step, flush)
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     sampler = ClockSampler(local)
@@ -269,6 +269,20 @@ def run_gpu(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def count_engine_launches(step, flush) -> int:
+    """Kernels of the engine's .so (namespace sr::) launched by one step, counted by CUPTI
+    (torch.profiler) outside the timed region."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    flush.fill_(0.0)
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        step()
+        torch.cuda.synchronize()
+    return sum(1 for ev in prof.events() if ev.device_type.name == "CUDA" and "sr::" in ev.name)
 
 
 def cpu_baseline(config: str, threads: int, budget_s: float = 15.0, evals: int | None = None):

@@ -116,7 +116,11 @@ class ShardedFieldObjective:
         return y_full[..., self.ylo:self.yhi].contiguous()
 
     def launches_per_step(self) -> int:
-        n = 5  # pass 1, CTA reduce, raw pack, finalize, pass 2
+        """Nominal engine launches per evaluate() (bench.py counts the real ones with CUPTI)."""
+        if self.whole:  # sr_evaluate: pass 1 (2 kernels for fp32 NCC, K in 17..32), reduce + finalize, pass 2
+            n = 3 + (1 if (self.feature == "ncc" and self.frames.data.dtype == torch.float32 and 17 <= self.k <= 32) else 0)
+        else:  # pass 1, CTA reduce, finalize, pass 2
+            n = 4
         if self.feature == "ngf":
             n += 1  # adjoint of the discrete gradient + chain rule
         return n
