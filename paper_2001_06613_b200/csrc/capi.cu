@@ -494,9 +494,9 @@ int sr_frame_shifts(sr_ctx* c, int32_t dtype, const void* frames, int32_t nframe
   if (!c || !frames || !shifts || nframes < 1 || n < 1) return fail(SR_ERR_ARG, "bad sr_frame_shifts arguments");
   CK(cudaSetDevice(c->device));
   if (dtype == SR_F32)
-    k_frame_mean<float><<<nframes, 256, 0, c->stream>>>((const float*)frames, n, (float*)shifts);
+    k_frame_mean<float><<<nframes, 1024, 0, c->stream>>>((const float*)frames, n, (float*)shifts);
   else
-    k_frame_mean<double><<<nframes, 256, 0, c->stream>>>((const double*)frames, n, (double*)shifts);
+    k_frame_mean<double><<<nframes, 1024, 0, c->stream>>>((const double*)frames, n, (double*)shifts);
   CK(cudaGetLastError());
   return SR_OK;
 }

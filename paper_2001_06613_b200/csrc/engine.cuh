@@ -1202,19 +1202,35 @@ __global__ void __launch_bounds__(256) k_interp_linear(int n, long long M, const
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256) k_frame_mean(const T* __restrict__ frames, long long N,
-                                                    T* __restrict__ out) {
-  __shared__ double red[8];
+__global__ void __launch_bounds__(1024) k_frame_mean(const T* __restrict__ frames, long long N,
+                                                     T* __restrict__ out) {
+  // one block per frame (fixed summation order: deterministic); 4 independent fp64 chains per
+  // thread over 16-byte loads when the frame is 16-byte aligned
+  __shared__ double red[32];
   const T* f = frames + (long long)blockIdx.x * N;
-  double s = 0.0;
-  for (long long i = threadIdx.x; i < N; i += blockDim.x) s += (double)f[i];
-  s = warp_sum(s);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
+  long long head = 0;
+  if (sizeof(T) == 4 && (reinterpret_cast<uintptr_t>(f) & 15) == 0) {
+    const long long n4 = N / 4;
+    const float4* f4 = reinterpret_cast<const float4*>(f);
+    for (long long i = threadIdx.x; i < n4; i += blockDim.x) {
+      const float4 v = __ldg(f4 + i);
+      s[0] += (double)v.x;
+      s[1] += (double)v.y;
+      s[2] += (double)v.z;
+      s[3] += (double)v.w;
+    }
+    head = n4 * 4;
+  }
+  for (long long i = head + threadIdx.x; i < N; i += blockDim.x) s[i & 3] += (double)f[i];
+  double t0 = (s[0] + s[1]) + (s[2] + s[3]);
+  t0 = warp_sum(t0);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t0;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int w = 0; w < 8; ++w) t += red[w];
-    out[blockIdx.x] = (T)(t / (double)N);
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) out[blockIdx.x] = (T)(v / (double)N);
   }
 }
 
