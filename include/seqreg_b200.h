@@ -64,6 +64,7 @@ extern "C" {
 #define SR_ERR_CUDA 2        /* CUDA runtime error (RuntimeError) */
 #define SR_ERR_SINGULAR 3    /* vanishing Thomas pivot (temporal.py:141-142 SingularSystemError) */
 #define SR_ERR_UNSUPPORTED 4 /* e.g. more than SR_MAX_FRAMES subset frames */
+#define SR_ERR_CALLBACK 5    /* a caller-supplied callback returned non-zero (its error is the caller's) */
 
 #define SR_MAX_FRAMES 128    /* subset size limit of the fused kernels */
 
@@ -192,6 +193,60 @@ SR_API int sr_ls_predict(sr_ctx* ctx, int32_t dtype, int32_t n, int64_t m, const
 SR_API int sr_interp_linear(sr_ctx* ctx, int32_t dtype, int32_t n, int64_t m, const int32_t* left,
                      const int32_t* right, const double* theta, const void* src_dev,
                      void* zeta_dev);
+
+/* ------------------------------------------------------------------ device L-BFGS
+ * lbfgs_minimize (optimizer.py:76-168) with every vector (x, g, the search direction,
+ * the m curvature pairs) resident in device memory as fp64.  Same algorithm: two-loop
+ * recursion (optimizer.py:59-73), Armijo backtracking only, curvature pairs with
+ * s.y <= 1e-10 |s| |y| clear the history, the five stop reasons.  Element-wise updates
+ * round like numpy (no FMA contraction); dot products use a fixed-order reduction
+ * (deterministic; their summation order differs from BLAS, so results agree with the
+ * reference to rounding, iteration counts and stop reasons match except on knife edges).
+ *
+ * The objective is a caller callback on device buffers:
+ *   objective(user, x_dev, &f, g_dev) -> 0 on success; x_dev, g_dev are [n] fp64 on the
+ *   context's device, valid for the duration of the call; the callback must have finished
+ *   writing g_dev when it returns (the driver synchronises its stream before the call).
+ * trace (optional) is called after every accepted step like optimizer.py:155-156. */
+typedef int (*sr_objective_fn)(void* user, const double* x_dev, double* f_out, double* g_dev);
+typedef void (*sr_trace_fn)(void* user, int32_t iteration, double f, double grad_inf, double step,
+                            int32_t evaluations);
+
+typedef struct sr_lbfgs_options { /* OptimOptions, optimizer.py:27-46 (same defaults) */
+  int32_t memory;           /* 5 */
+  int32_t max_iters;        /* 50 */
+  double grad_tol;          /* 1e-4, on |g|_inf relative to the first iterate */
+  double step_tol;          /* 1e-7 */
+  double f_tol;             /* 1e-5, on the accepted decrease relative to 1 + |f| */
+  double armijo_c1;         /* 1e-4 */
+  double backtrack_factor;  /* 0.5 */
+  int32_t max_backtracks;   /* 20 */
+} sr_lbfgs_options;
+
+#define SR_LBFGS_GRAD_TOL 0
+#define SR_LBFGS_STEP_TOL 1
+#define SR_LBFGS_F_TOL 2
+#define SR_LBFGS_MAX_ITERS 3
+#define SR_LBFGS_LINE_SEARCH_FAILURE 4
+
+typedef struct sr_lbfgs_result { /* OptimResult, optimizer.py:49-56 (x_final is x_dev itself) */
+  double f_final;
+  double f_initial;
+  int32_t iterations;
+  int32_t objective_evaluations;
+  int32_t converged_reason; /* SR_LBFGS_* */
+} sr_lbfgs_result;
+
+/* Fills `opts` with the reference defaults. */
+SR_API void sr_lbfgs_defaults(sr_lbfgs_options* opts);
+
+/* Minimise from x_dev (in: x0, out: the final iterate), n >= 1 parameters.  Returns
+ * SR_ERR_ARG for invalid options (optimizer.py:38-46 messages) or a non-finite objective at
+ * the start ("objective is not finite at the starting point"), SR_ERR_CALLBACK when the
+ * objective returns non-zero.  Synchronous (returns after the last evaluation). */
+SR_API int sr_lbfgs_minimize(sr_ctx* ctx, int64_t n, double* x_dev, const sr_lbfgs_options* opts,
+                             sr_objective_fn objective, void* objective_user, sr_trace_fn trace,
+                             void* trace_user, sr_lbfgs_result* result);
 
 #ifdef __cplusplus
 }

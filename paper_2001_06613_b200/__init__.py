@@ -17,6 +17,7 @@ from ._lib import EngineUnavailable, SingularSystemError, load_library
 from .datatypes import Affine, AffineStack, Grid, Image, ImageSequence, identity_affine, identity_params
 from .engine import DeviceFrames, Engine, EvalPlan, GridSpec, get_engine
 from .field import FieldObjective
+from .optimizer import ObjectiveEval, OptimOptions, OptimResult, lbfgs_minimize
 from .similarity import (
     CorrelationState,
     configure,
@@ -59,5 +60,9 @@ __all__ = [
     "load_library",
     "ls_predict_fields",
     "min_consecutive_rho",
+    "ObjectiveEval",
+    "OptimOptions",
+    "OptimResult",
+    "lbfgs_minimize",
     "uninstall",
 ]

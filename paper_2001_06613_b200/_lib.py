@@ -19,6 +19,11 @@ __all__ = [
     "SR_ERR_CUDA",
     "SR_ERR_SINGULAR",
     "SR_ERR_UNSUPPORTED",
+    "SR_ERR_CALLBACK",
+    "SrLbfgsOptions",
+    "SrLbfgsResult",
+    "OBJECTIVE_FN",
+    "TRACE_FN",
     "SR_F32",
     "SR_F64",
     "SR_NCC",
@@ -34,7 +39,7 @@ __all__ = [
     "check",
 ]
 
-SR_OK, SR_ERR_ARG, SR_ERR_CUDA, SR_ERR_SINGULAR, SR_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
+SR_OK, SR_ERR_ARG, SR_ERR_CUDA, SR_ERR_SINGULAR, SR_ERR_UNSUPPORTED, SR_ERR_CALLBACK = 0, 1, 2, 3, 4, 5
 SR_F32, SR_F64 = 0, 1
 SR_NCC, SR_NGF = 0, 1
 SR_AFFINE, SR_DISPLACEMENT = 0, 1
@@ -77,6 +82,35 @@ class SrProblem(ctypes.Structure):
     ]
 
 
+class SrLbfgsOptions(ctypes.Structure):
+    _fields_ = [
+        ("memory", ctypes.c_int32),
+        ("max_iters", ctypes.c_int32),
+        ("grad_tol", ctypes.c_double),
+        ("step_tol", ctypes.c_double),
+        ("f_tol", ctypes.c_double),
+        ("armijo_c1", ctypes.c_double),
+        ("backtrack_factor", ctypes.c_double),
+        ("max_backtracks", ctypes.c_int32),
+    ]
+
+
+class SrLbfgsResult(ctypes.Structure):
+    _fields_ = [
+        ("f_final", ctypes.c_double),
+        ("f_initial", ctypes.c_double),
+        ("iterations", ctypes.c_int32),
+        ("objective_evaluations", ctypes.c_int32),
+        ("converged_reason", ctypes.c_int32),
+    ]
+
+
+# objective(user, x_dev, f_out, g_dev) -> status; trace(user, iteration, f, grad_inf, step, evaluations)
+OBJECTIVE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
+                                ctypes.c_void_p)
+TRACE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int32, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                            ctypes.c_int32)
+
 _c = ctypes
 _P = ctypes.c_void_p
 _D = ctypes.POINTER(ctypes.c_double)
@@ -114,6 +148,11 @@ EXPORTS = {
     "sr_interp_linear": (
         _c.c_int,
         [_P, _c.c_int32, _c.c_int32, _c.c_int64, _I32P, _I32P, _D, _P, _P],
+    ),
+    "sr_lbfgs_defaults": (None, [_c.POINTER(SrLbfgsOptions)]),
+    "sr_lbfgs_minimize": (
+        _c.c_int,
+        [_P, _c.c_int64, _P, _c.POINTER(SrLbfgsOptions), OBJECTIVE_FN, _P, TRACE_FN, _P, _c.POINTER(SrLbfgsResult)],
     ),
 }
 

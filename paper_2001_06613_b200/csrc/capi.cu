@@ -23,6 +23,16 @@ struct TexSet {
   std::vector<cudaTextureObject_t> tex;
 };
 
+namespace sr {
+namespace lbfgs {
+struct Workspace;
+int minimize(Workspace*& wsp, cudaStream_t st, int sms, long long n, double* x, const sr_lbfgs_options& o,
+             sr_objective_fn objective, void* ouser, sr_trace_fn trace, void* tuser, sr_lbfgs_result* res,
+             char* err, size_t errlen);
+void destroy(Workspace* w);
+}  // namespace lbfgs
+}  // namespace sr
+
 struct sr_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -44,6 +54,7 @@ struct sr_ctx {
   double* part = nullptr;
   size_t part_cap = 0;  // doubles
   unsigned* ticket = nullptr;  // last-block ticket of k_reduce_finalize
+  sr::lbfgs::Workspace* lbfgs = nullptr;  // device L-BFGS vectors (lbfgs.cu)
   void* zbuf = nullptr;
   size_t zbuf_bytes = 0;
   double* aux = nullptr;  // small device scratch (temporal factors, S partial reduce)
@@ -393,6 +404,7 @@ int sr_destroy(sr_ctx* c) {
   cudaFreeHost(c->job_host);
   cudaFree(c->part);
   cudaFree(c->ticket);
+  sr::lbfgs::destroy(c->lbfgs);
   cudaFree(c->vbuf);
   for (auto& t : c->texsets) texset_free(t);
   cudaFree(c->zbuf);
@@ -701,6 +713,37 @@ int sr_interp_linear(sr_ctx* c, int32_t dtype, int32_t n, int64_t m, const int32
     k_interp_linear<double><<<grid, 256, 0, c->stream>>>(n, m, c->iaux, c->iaux + n, c->aux, (const double*)src, (double*)zeta);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(c->stream));
+  return SR_OK;
+}
+
+void sr_lbfgs_defaults(sr_lbfgs_options* o) {
+  if (!o) return;
+  o->memory = 5;
+  o->max_iters = 50;
+  o->grad_tol = 1e-4;
+  o->step_tol = 1e-7;
+  o->f_tol = 1e-5;
+  o->armijo_c1 = 1e-4;
+  o->backtrack_factor = 0.5;
+  o->max_backtracks = 20;
+}
+
+int sr_lbfgs_minimize(sr_ctx* c, int64_t n, double* x_dev, const sr_lbfgs_options* o, sr_objective_fn objective,
+                      void* objective_user, sr_trace_fn trace, void* trace_user, sr_lbfgs_result* result) {
+  if (!c || !x_dev || !o || !objective || !result) return fail(SR_ERR_ARG, "null argument");
+  if (n < 1) return fail(SR_ERR_ARG, "n must be >= 1");
+  // OptimOptions.__post_init__ (optimizer.py:38-46)
+  if (o->memory < 1 || o->max_iters < 1 || o->max_backtracks < 1)
+    return fail(SR_ERR_ARG, "memory, max_iters, max_backtracks must be >= 1");
+  if (!(o->grad_tol > 0) || !(o->step_tol > 0) || !(o->f_tol > 0)) return fail(SR_ERR_ARG, "tolerances must be > 0");
+  if (!(o->armijo_c1 > 0 && o->armijo_c1 < 1)) return fail(SR_ERR_ARG, "armijo_c1 must be in (0, 1)");
+  if (!(o->backtrack_factor > 0 && o->backtrack_factor < 1))
+    return fail(SR_ERR_ARG, "backtrack_factor must be in (0, 1)");
+  CK(cudaSetDevice(c->device));
+  char err[256] = {0};
+  const int rc = sr::lbfgs::minimize(c->lbfgs, c->stream, c->sms, n, x_dev, *o, objective, objective_user, trace,
+                                     trace_user, result, err, sizeof err);
+  if (rc) return fail(rc, "%s", err);
   return SR_OK;
 }
 
