@@ -194,6 +194,23 @@ SR_API int sr_interp_linear(sr_ctx* ctx, int32_t dtype, int32_t n, int64_t m, co
                      const int32_t* right, const double* theta, const void* src_dev,
                      void* zeta_dev);
 
+/* ------------------------------------------------------------------ spatial hierarchy
+ * One pyramid step for every frame of a stack (pyramid.py:22-54; build_pyramid 68-91 applies it
+ * level by level): dst = restrict(smooth(src)).  smooth = separable [1,2,1]/4 with reflective
+ * boundaries (scipy.ndimage.convolve1d mode="reflect"), restrict = block means of 2^ndim cells with
+ * a smaller trailing block on odd axes.  src_dev [nframes][prod(dims)], dst_dev
+ * [nframes][prod(ceil(dims/2))]; the coarse grid has doubled spacing and the same origin.
+ * fp64 results are bit-identical to the reference. */
+SR_API int sr_pyramid_step(sr_ctx* ctx, int32_t dtype, int32_t ndim, const int32_t* dims, int32_t nframes,
+                           const void* src_dev, void* dst_dev);
+
+/* Spatial prolongation of displacement fields (absent in the reference): yc_dev
+ * [k][ndim][N_coarse] absolute positions on `coarse` -> yf_dev [k][ndim][N_fine] on `fine`, by
+ * multilinear interpolation of u = y - x at the fine cell centres, coordinates clamped to the hull
+ * of the coarse centres (edge replication), y_fine = x_fine + u. */
+SR_API int sr_prolong_field(sr_ctx* ctx, int32_t dtype, const sr_grid* coarse, const sr_grid* fine, int32_t k,
+                            const void* yc_dev, void* yf_dev);
+
 /* ------------------------------------------------------------------ device L-BFGS
  * lbfgs_minimize (optimizer.py:76-168) with every vector (x, g, the search direction,
  * the m curvature pairs) resident in device memory as fp64.  Same algorithm: two-loop

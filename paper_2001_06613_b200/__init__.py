@@ -29,6 +29,7 @@ from .similarity import (
     min_consecutive_rho,
     uninstall,
 )
+from .spatial import build_pyramid, prolong_field, pyramid_step
 from .temporal import interp_linear_fields, ls_predict_fields
 
 __version__ = "0.1.0"
@@ -64,5 +65,8 @@ __all__ = [
     "OptimOptions",
     "OptimResult",
     "lbfgs_minimize",
+    "build_pyramid",
+    "prolong_field",
+    "pyramid_step",
     "uninstall",
 ]

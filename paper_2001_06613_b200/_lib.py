@@ -149,6 +149,8 @@ EXPORTS = {
         _c.c_int,
         [_P, _c.c_int32, _c.c_int32, _c.c_int64, _I32P, _I32P, _D, _P, _P],
     ),
+    "sr_pyramid_step": (_c.c_int, [_P, _c.c_int32, _c.c_int32, _I32P, _c.c_int32, _P, _P]),
+    "sr_prolong_field": (_c.c_int, [_P, _c.c_int32, _c.POINTER(SrGrid), _c.POINTER(SrGrid), _c.c_int32, _P, _P]),
     "sr_lbfgs_defaults": (None, [_c.POINTER(SrLbfgsOptions)]),
     "sr_lbfgs_minimize": (
         _c.c_int,

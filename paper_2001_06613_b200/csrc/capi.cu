@@ -11,6 +11,7 @@
 
 #include "../../include/seqreg_b200.h"
 #include "launch.cuh"
+#include "pyramid.cuh"
 
 using namespace sr;
 
@@ -713,6 +714,58 @@ int sr_interp_linear(sr_ctx* c, int32_t dtype, int32_t n, int64_t m, const int32
     k_interp_linear<double><<<grid, 256, 0, c->stream>>>(n, m, c->iaux, c->iaux + n, c->aux, (const double*)src, (double*)zeta);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(c->stream));
+  return SR_OK;
+}
+
+int sr_pyramid_step(sr_ctx* c, int32_t dtype, int32_t ndim, const int32_t* dims, int32_t nframes,
+                    const void* src_dev, void* dst_dev) {
+  if (!c || !dims || !src_dev || !dst_dev) return fail(SR_ERR_ARG, "null argument");
+  if (ndim < 1 || ndim > 3 || nframes < 1) return fail(SR_ERR_ARG, "bad ndim/nframes");
+  if (dtype != SR_F32 && dtype != SR_F64) return fail(SR_ERR_ARG, "bad dtype");
+  PyrDims f{ndim, {1, 1, 1}, 1}, cg{ndim, {1, 1, 1}, 1};
+  for (int a = 0; a < ndim; ++a) {
+    if (dims[a] < 1) return fail(SR_ERR_ARG, "dims must be >= 1");
+    f.n[a] = dims[a];
+    cg.n[a] = (dims[a] + 1) / 2;  // ceil(dims / 2) (pyramid.py:48)
+    f.N *= dims[a];
+    cg.N *= cg.n[a];
+  }
+  CK(cudaSetDevice(c->device));
+  if (cg.n[1] * cg.n[2] > 65535 || nframes > 65535 || f.N > (1LL << 31)) return fail(SR_ERR_ARG, "stack too large");
+  const dim3 grid((unsigned)((cg.n[0] + 127) / 128), (unsigned)(cg.n[1] * cg.n[2]), (unsigned)nframes);
+  if (dtype == SR_F32) {
+    if (ndim == 3) k_pyramid<float, true><<<grid, 128, 0, c->stream>>>((const float*)src_dev, (float*)dst_dev, f, cg);
+    else k_pyramid<float, false><<<grid, 128, 0, c->stream>>>((const float*)src_dev, (float*)dst_dev, f, cg);
+  } else {
+    if (ndim == 3) k_pyramid<double, true><<<grid, 128, 0, c->stream>>>((const double*)src_dev, (double*)dst_dev, f, cg);
+    else k_pyramid<double, false><<<grid, 128, 0, c->stream>>>((const double*)src_dev, (double*)dst_dev, f, cg);
+  }
+  CK(cudaGetLastError());
+  return SR_OK;
+}
+
+int sr_prolong_field(sr_ctx* c, int32_t dtype, const sr_grid* coarse, const sr_grid* fine, int32_t k,
+                     const void* yc_dev, void* yf_dev) {
+  if (!c || !coarse || !fine || !yc_dev || !yf_dev) return fail(SR_ERR_ARG, "null argument");
+  if (k < 1 || coarse->ndim != fine->ndim || coarse->ndim < 2 || coarse->ndim > 3)
+    return fail(SR_ERR_ARG, "bad k / ndim");
+  if (dtype != SR_F32 && dtype != SR_F64) return fail(SR_ERR_ARG, "bad dtype");
+  for (int a = 0; a < coarse->ndim; ++a)
+    if (coarse->dims[a] < 2 || fine->dims[a] < 1 || !(coarse->spacing[a] > 0) || !(fine->spacing[a] > 0))
+      return fail(SR_ERR_ARG, "coarse dims must be >= 2 and spacings > 0");
+  CK(cudaSetDevice(c->device));
+  const Geo gc = make_geo(*coarse), gf = make_geo(*fine);
+  if (gf.N > (1LL << 31) || gc.N > (1LL << 31)) return fail(SR_ERR_ARG, "grid too large");
+  constexpr int FG = 4;  // frames per thread
+  const dim3 grid((unsigned)((gf.N + 255) / 256), (unsigned)((k + FG - 1) / FG));
+  if (dtype == SR_F32) {
+    if (gf.nd == 2) k_prolong_field<float, 2, FG><<<grid, 256, 0, c->stream>>>((const float*)yc_dev, (float*)yf_dev, gc, gf, k);
+    else k_prolong_field<float, 3, FG><<<grid, 256, 0, c->stream>>>((const float*)yc_dev, (float*)yf_dev, gc, gf, k);
+  } else {
+    if (gf.nd == 2) k_prolong_field<double, 2, FG><<<grid, 256, 0, c->stream>>>((const double*)yc_dev, (double*)yf_dev, gc, gf, k);
+    else k_prolong_field<double, 3, FG><<<grid, 256, 0, c->stream>>>((const double*)yc_dev, (double*)yf_dev, gc, gf, k);
+  }
+  CK(cudaGetLastError());
   return SR_OK;
 }
 
