@@ -63,8 +63,13 @@ class OptimOptions:
             raise ValueError("backtrack_factor must be in (0, 1)")
 
     def c_struct(self) -> _lib.SrLbfgsOptions:
-        return _lib.SrLbfgsOptions(self.memory, self.max_iters, self.grad_tol, self.step_tol, self.f_tol,
-                                   self.armijo_c1, self.backtrack_factor, self.max_backtracks)
+        return _c_options(self)
+
+
+def _c_options(o) -> _lib.SrLbfgsOptions:
+    """Any options object with the OptimOptions fields (ours or the reference's own)."""
+    return _lib.SrLbfgsOptions(int(o.memory), int(o.max_iters), float(o.grad_tol), float(o.step_tol),
+                               float(o.f_tol), float(o.armijo_c1), float(o.backtrack_factor), int(o.max_backtracks))
 
 
 @dataclass
@@ -100,6 +105,9 @@ def lbfgs_minimize(objective, x0, opts: OptimOptions | None = None, trace=None, 
     """
     if opts is None:
         opts = OptimOptions()
+    elif not isinstance(opts, OptimOptions):  # e.g. the reference's own OptimOptions: same fields, same checks
+        opts = OptimOptions(*(getattr(opts, f) for f in ("memory", "max_iters", "grad_tol", "step_tol", "f_tol",
+                                                          "armijo_c1", "backtrack_factor", "max_backtracks")))
     eng = engine if engine is not None else get_engine()
     dev = eng.device
     device_mode = isinstance(x0, torch.Tensor) and x0.is_cuda
@@ -139,7 +147,7 @@ def lbfgs_minimize(objective, x0, opts: OptimOptions | None = None, trace=None, 
     tcb = _lib.TRACE_FN(_trace) if trace is not None else _lib.TRACE_FN()
     res = _lib.SrLbfgsResult()
     torch.cuda.synchronize(dev)
-    status = eng.lib.sr_lbfgs_minimize(eng.ctx, n, ctypes.c_void_p(x_t.data_ptr()), ctypes.byref(opts.c_struct()),
+    status = eng.lib.sr_lbfgs_minimize(eng.ctx, n, ctypes.c_void_p(x_t.data_ptr()), ctypes.byref(_c_options(opts)),
                                        ocb, None, tcb, None, ctypes.byref(res))
     if errors:
         raise errors[0]

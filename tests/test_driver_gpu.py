@@ -50,3 +50,34 @@ def test_reference_driver_on_gpu_matches_cpu(method):
         assert rg.dissim_all == pytest.approx(rc.dissim_all, rel=1e-8)
     a, b = stack_cpu.params_matrix(), stack_gpu.params_matrix()
     assert np.abs(a - b).max() <= 1e-8 * max(1.0, np.abs(a).max())
+
+
+@pytest.mark.parametrize("method", ["spml", "stml"])
+def test_reference_driver_with_device_lbfgs(method):
+    """The reference drivers with both the evaluation (install()) and the optimizer
+    (seqreg.temporal.lbfgs_minimize -> the device L-BFGS, host mode) replaced: same iteration /
+    evaluation counts, stop reasons and final objective as the CPU reference."""
+    import seqreg.temporal as T
+
+    from paper_2001_06613_b200 import optimizer as dev_opt
+
+    seq, truth = seqreg.synth_generate(seqreg.SynthSpec(dims=(48, 40), frames=9, seed=4))
+    opts = seqreg.OptimOptions(max_iters=8, grad_tol=1e-30, step_tol=1e-30, f_tol=1e-30)
+    cfg = seqreg.RunConfig(spatial_levels=2, temporal_coarsest_size=3, optim=opts)
+    stack_cpu, runs_cpu = _run(method, seq, cfg)
+    srb.configure(dtype=torch.float64, feature="ncc")
+    srb.install()
+    saved = T.lbfgs_minimize
+    T.lbfgs_minimize = dev_opt.lbfgs_minimize
+    try:
+        stack_gpu, runs_gpu = _run(method, seq, cfg)
+    finally:
+        T.lbfgs_minimize = saved
+        srb.uninstall()
+    assert len(runs_cpu) == len(runs_gpu)
+    for rc, rg in zip(runs_cpu, runs_gpu):
+        assert (rc.result.iterations, rc.result.objective_evaluations, rc.result.converged_reason) == (
+            rg.result.iterations, rg.result.objective_evaluations, rg.result.converged_reason)
+        assert rg.result.f_final == pytest.approx(rc.result.f_final, rel=1e-8)
+    a, b = stack_cpu.params_matrix(), stack_gpu.params_matrix()
+    assert np.abs(a - b).max() <= 1e-7 * max(1.0, np.abs(a).max())
