@@ -40,6 +40,15 @@ def bytes_per_vf(d: int, s: int) -> dict:
     return {"pass1": (1 + d) * s, "pass2": (1 + 2 * d) * s, "eval": (2 + 3 * d) * s}
 
 
+# compulsory bytes per voxel-frame of each engine kernel as designed: the split pass 1
+# writes V (s) and grad T (d s) next to its y + T reads; the streaming pass 2 reads them back and
+# writes dD/dy; the fused kernels move exactly the SURVEY §8d pass figures
+def kernel_bytes_per_vf(d: int, s: int) -> dict:
+    return {"k_sample_v": 2 * (1 + d) * s, "k_gram_tc": s, "k_pass2_stream": (1 + 2 * d) * s,
+            "k_pass2": (1 + 2 * d) * s, "k_pass1_tc": (1 + d) * s, "k_pass1_ws": (1 + d) * s, "k_pass1": (1 + d) * s,
+            "k_reduce_finalize": 0}
+
+
 def _peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -183,7 +192,7 @@ def run_gpu(args):
         flush.fill_(1.0)
         step()
     torch.cuda.synchronize()
-    launches_per_step = count_engine_launches(step, flush)
+    launches_per_step, kdev = engine_kernel_times(step, flush, reps=max(5, min(args.steps, 20)))
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     sampler = ClockSampler(local)
@@ -211,13 +220,17 @@ def run_gpu(args):
     vf_total = N * K
     value = vf_total / (ms_step * 1e-3)
 
-    # ---- per-kernel roofline (pass 1 incl. its CTA reduce, finalize, pass 2), CUDA events on the stream
+    # ---- roofline.  Phases by CUDA events on the launching stream (pass 1 = its kernels + CTA reduce,
+    # finalize, pass 2 = one kernel); per kernel by CUPTI device time over the same flushed loop.  The
+    # dominant kernel is the longest one; its bytes are its compulsory traffic per voxel-frame.
     rl = obj.kernel_times(y, grad, flush, reps=max(5, min(args.steps, 50)))
     s = 4 if cfg.dtype == torch.float32 else 8
     bpv = bytes_per_vf(d, s)
+    kbv = kernel_bytes_per_vf(d, s)
     peak, peak_src = _peaks()
-    kern = "pass2" if rl["pass2"] >= rl["pass1"] else "pass1"
-    achieved = bpv[kern] * vf_rank / (rl[kern] * 1e-3) / 1e9
+    kern = max(kdev, key=kdev.get)
+    kern_ms = kdev[kern]
+    achieved = kbv.get(kern, 0) * vf_rank / (kern_ms * 1e-3) / 1e9
     eval_achieved = bpv["eval"] * vf_rank / (ms_step * 1e-3) / 1e9
     traffic = None
     prof = ROOT / "profiles" / f"traffic_{args.config}.json"
@@ -257,9 +270,10 @@ def run_gpu(args):
                        "l2": "flushed before every timed step (256 MiB write + 256 MiB read, outside the event window)"},
             "roofline": {"bound": "hbm", "kernel": kern, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "bytes_per_vf": bpv[kern], "kernel_ms": rl[kern],
+                         "bytes_per_vf": kbv.get(kern, 0), "kernel_ms": kern_ms, "kernel_timing": "CUPTI device time",
+                         "kernels_ms": kdev, "kernels_bytes_per_vf": {k: kbv.get(k, 0) for k in kdev},
                          "eval_achieved": eval_achieved, "eval_frac": eval_achieved / peak,
-                         "eval_bytes_per_vf": bpv["eval"], "kernel_ms_all": rl},
+                         "eval_bytes_per_vf": bpv["eval"], "phases_ms_events": rl},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
@@ -271,18 +285,25 @@ def run_gpu(args):
         dist.destroy_process_group()
 
 
-def count_engine_launches(step, flush) -> int:
-    """Kernels of the engine's .so (namespace sr::) launched by one step, counted by CUPTI
-    (torch.profiler) outside the timed region."""
+def engine_kernel_times(step, flush, reps: int = 10):
+    """Kernels of the engine's .so (namespace sr::) per step and their mean CUPTI device time (ms),
+    over ``reps`` steps with the L2 flush in between, outside the timed region."""
     import torch
     from torch.profiler import ProfilerActivity, profile
 
-    flush.fill_(0.0)
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
-        step()
+        for i in range(reps):
+            flush.fill_(float(i))
+            step()
         torch.cuda.synchronize()
-    return sum(1 for ev in prof.events() if ev.device_type.name == "CUDA" and "sr::" in ev.name)
+    times, count = {}, 0
+    for ev in prof.events():
+        if ev.device_type.name == "CUDA" and "sr::" in ev.name:
+            count += 1
+            base = ev.name.replace("void ", "").replace("sr::", "").split("<")[0].split("(")[0].strip()
+            times.setdefault(base, []).append(ev.device_time * 1e-3)
+    return count // reps, {k: float(sum(v) / len(v)) for k, v in times.items()}
 
 
 def cpu_baseline(config: str, threads: int, budget_s: float = 15.0, evals: int | None = None):

@@ -134,6 +134,12 @@ SR_API int sr_destroy(sr_ctx* ctx);
 SR_API int sr_set_stream(sr_ctx* ctx, void* stream);
 /* Number of CTAs the persistent kernels launch (defaults to a multiple of the SM count). */
 SR_API int sr_set_grid_ctas(sr_ctx* ctx, int32_t ctas);
+/* Allow sr_grad to reuse the per-sample values and interpolant gradients that the preceding
+ * sr_corr_partial on this context cached for the same problem (same y pointer, slab, frames and
+ * subset), instead of re-gathering them.  Enable only when y is not modified between the two calls
+ * (the reference's D + grad D pattern); sr_evaluate always reuses within its own call.
+ * Default: off. */
+SR_API int sr_set_sample_reuse(sr_ctx* ctx, int32_t enable);
 
 /* Prepare an fp32 frame stack for the texture-gather sampling path: the frames are copied
  * once into gather-capable CUDA arrays (block-linear; 3-D frames as stacked z-slices) cached

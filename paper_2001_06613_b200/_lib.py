@@ -130,6 +130,7 @@ EXPORTS = {
     "sr_destroy": (_c.c_int, [_P]),
     "sr_set_stream": (_c.c_int, [_P, _P]),
     "sr_set_grid_ctas": (_c.c_int, [_P, _c.c_int32]),
+    "sr_set_sample_reuse": (_c.c_int, [_P, _c.c_int32]),
     "sr_frame_shifts": (_c.c_int, [_P, _c.c_int32, _P, _c.c_int32, _c.c_int64, _P]),
     "sr_frames_prepare": (_c.c_int, [_P, _c.c_int32, _P, _c.c_int32, _c.POINTER(SrGrid)]),
     "sr_frames_release": (_c.c_int, [_P, _P]),

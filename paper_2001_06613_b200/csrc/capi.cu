@@ -48,6 +48,19 @@ struct sr_ctx {
   int split = 1;   // SEQREG_B200_SPLIT=0: fused tensor-core pass 1 instead of sampling kernel + Gram kernel
   float* vbuf = nullptr;  // split pass 1: V = v - shift, [K][vstride]
   size_t vbuf_bytes = 0;
+  float* gbuf = nullptr;  // split pass 1 with the streaming pass 2: grad T, [K][d][vstride]
+  size_t gbuf_bytes = 0;
+  int p2s = 1;            // SEQREG_B200_P2S=0: re-gathering pass 2 instead of the streaming pass 2
+  int sample_reuse = 0;   // sr_set_sample_reuse: sr_grad may reuse the samples of the last sr_corr_partial
+  // what vbuf / gbuf hold: the samples of this (y, slab, frames, subset); pass 2 reuses them on a match
+  struct VTag {
+    int valid = 0, k = 0, ndim = 0, has_g = 0;
+    const void* y = nullptr;
+    const void* frames = nullptr;
+    const void* shifts = nullptr;
+    int64_t y_off = 0, y_stride = 0, pix_lo = 0, pix_hi = 0, vstride = 0;
+    int frame_index[SR_MAX_FRAMES];
+  } vtag;
   Job* job_dev = nullptr;
   Job* job_host = nullptr;  // pinned staging
   Job job_last{};           // content of the last upload (skip identical re-uploads)
@@ -275,6 +288,36 @@ static int pass1_kp(const sr_ctx* c, const sr_problem* p) {
   return kp_of(p->k);
 }
 
+static void set_vtag(sr_ctx* c, const sr_problem* p, long long vstride, int has_g) {
+  sr_ctx::VTag& t = c->vtag;
+  t.valid = 1;
+  t.k = p->k;
+  t.ndim = p->grid.ndim;
+  t.has_g = has_g;
+  t.y = p->y_dev;
+  t.frames = p->frames_dev;
+  t.shifts = p->shifts_dev;
+  t.y_off = p->y_off;
+  t.y_stride = p->y_stride;
+  t.pix_lo = p->pix_lo;
+  t.pix_hi = p->pix_hi;
+  t.vstride = vstride;
+  for (int k = 0; k < p->k; ++k) t.frame_index[k] = p->frame_index[k];
+}
+
+// pass 2 may reuse vbuf / gbuf: same y buffer, slab, frames and subset as the last split pass 1
+// (the caller's contract: sr_grad follows the sr_corr_* calls at the same y)
+static bool vtag_matches(const sr_ctx* c, const sr_problem* p) {
+  const sr_ctx::VTag& t = c->vtag;
+  if (!t.valid || !t.has_g || t.k != p->k || t.ndim != p->grid.ndim || t.y != p->y_dev ||
+      t.frames != p->frames_dev || t.shifts != p->shifts_dev || t.y_off != p->y_off || t.y_stride != p->y_stride ||
+      t.pix_lo != p->pix_lo || t.pix_hi != p->pix_hi)
+    return false;
+  for (int k = 0; k < p->k; ++k)
+    if (t.frame_index[k] != p->frame_index[k]) return false;
+  return true;
+}
+
 static int corr_partial_impl(sr_ctx* c, const sr_problem* p, double* raw, double h = 0.0,
                              double* stats = nullptr) {
   const int KP = pass1_kp(c, p);
@@ -293,9 +336,20 @@ static int corr_partial_impl(sr_ctx* c, const sr_problem* p, double* raw, double
     rc = ensure(&vb, &c->vbuf_bytes, (size_t)p->k * vstride * 4);
     if (rc) return rc;
     c->vbuf = (float*)vb;
-    if (p->grid.ndim == 2) CK(pass1_split_d2(L, a, c->vbuf, vstride, c->part, c->part_cap, &nblk));
-    else CK(pass1_split_d3(L, a, c->vbuf, vstride, c->part, c->part_cap, &nblk));
+    float* G = nullptr;
+    if (c->p2s) {
+      void* gb = c->gbuf;
+      rc = ensure(&gb, &c->gbuf_bytes, (size_t)p->k * p->grid.ndim * vstride * 4);
+      if (rc) return rc;
+      c->gbuf = (float*)gb;
+      G = c->gbuf;
+    }
+    c->vtag.valid = 0;
+    if (p->grid.ndim == 2) CK(pass1_split_d2(L, a, c->vbuf, G, vstride, c->part, c->part_cap, &nblk));
+    else CK(pass1_split_d3(L, a, c->vbuf, G, vstride, c->part, c->part_cap, &nblk));
+    set_vtag(c, p, vstride, G != nullptr);
   } else {
+    c->vtag.valid = 0;
     CK(SR_SWITCH(p->dtype, p->grid.ndim, pass1, p->feature, p->param, KP, L, a, c->part, c->part_cap, &nblk));
   }
   const long long count = (long long)(p->pix_hi - p->pix_lo);
@@ -385,6 +439,8 @@ int sr_create(int32_t device, sr_ctx** out) {
     c->tc = (tcs && tcs[0] == '0') ? 0 : 1;
     const char* sp = getenv("SEQREG_B200_SPLIT");
     c->split = (sp && sp[0] == '0') ? 0 : 1;
+    const char* ps = getenv("SEQREG_B200_P2S");
+    c->p2s = (ps && ps[0] == '0') ? 0 : 1;
     const char* t2 = getenv("SEQREG_B200_TC2");
     c->tc2 = (t2 && t2[0] == '1') ? 1 : 0;
   }
@@ -407,6 +463,7 @@ int sr_destroy(sr_ctx* c) {
   cudaFree(c->ticket);
   sr::lbfgs::destroy(c->lbfgs);
   cudaFree(c->vbuf);
+  cudaFree(c->gbuf);
   for (auto& t : c->texsets) texset_free(t);
   cudaFree(c->zbuf);
   cudaFree(c->aux);
@@ -418,6 +475,12 @@ int sr_destroy(sr_ctx* c) {
 int sr_set_stream(sr_ctx* c, void* stream) {
   if (!c) return fail(SR_ERR_ARG, "null context");
   c->stream = (cudaStream_t)stream;
+  return SR_OK;
+}
+
+int sr_set_sample_reuse(sr_ctx* c, int32_t enable) {
+  if (!c) return fail(SR_ERR_ARG, "null context");
+  c->sample_reuse = enable ? 1 : 0;
   return SR_OK;
 }
 
@@ -537,7 +600,7 @@ int sr_corr_finalize(sr_ctx* c, const sr_problem* p, const double* raw_dev, cons
 }
 
 static int grad_impl(sr_ctx* c, const sr_problem* p, const double* stats, void* grad, int64_t g_off,
-                     int64_t g_stride) {
+                     int64_t g_stride, bool reuse) {
   const int KP = kp_of(p->k);
   const int d = p->grid.ndim, na = d * d + d;
   const Launch L = launch_of(c);
@@ -555,6 +618,11 @@ static int grad_impl(sr_ctx* c, const sr_problem* p, const double* stats, void* 
     a.out = grad;
     a.o_off = g_off;
     a.o_stride = g_stride;
+    if (reuse && p->dtype == SR_F32 && p->param == SR_DISPLACEMENT && p->k <= 32 && vtag_matches(c, p)) {
+      CK(d == 2 ? pass2_stream_d2(L, a, c->vbuf, c->gbuf, c->vtag.vstride)
+                : pass2_stream_d3(L, a, c->vbuf, c->gbuf, c->vtag.vstride));
+      return SR_OK;
+    }
     CK(SR_SWITCH(p->dtype, d, pass2, p->feature, p->param, KP, L, a, c->aux, c->aux_cap, &nblk));
     if (p->param == SR_AFFINE) {
       const int warps = p->k * na;
@@ -599,7 +667,7 @@ int sr_grad(sr_ctx* c, const sr_problem* p, const double* stats_dev, void* grad_
   CK(cudaSetDevice(c->device));
   rc = upload_job(c, p, nullptr);
   if (rc) return rc;
-  return grad_impl(c, p, stats_dev, grad_dev, g_off, g_stride);
+  return grad_impl(c, p, stats_dev, grad_dev, g_off, g_stride, c->sample_reuse != 0);
 }
 
 int sr_evaluate(sr_ctx* c, const sr_problem* p, const double* weights, double cell_volume,
@@ -615,7 +683,7 @@ int sr_evaluate(sr_ctx* c, const sr_problem* p, const double* weights, double ce
   rc = corr_partial_impl(c, p, raw_dev, cell_volume, stats_dev);
   if (rc) return rc;
   if (!grad_dev) return SR_OK;
-  return grad_impl(c, p, stats_dev, grad_dev, p->y_off, p->param == SR_DISPLACEMENT ? p->y_stride : 0);
+  return grad_impl(c, p, stats_dev, grad_dev, p->y_off, p->param == SR_DISPLACEMENT ? p->y_stride : 0, true);
 }
 
 int sr_curvature(sr_ctx* c, const sr_problem* p, double alpha, double h, void* grad, int64_t g_off,

@@ -267,8 +267,11 @@ namespace sr {
 // Thread = 4 pixels (lane-consecutive, stride 256) of one subset frame; writes the shifted
 // value v - shift to V[k][p - pix_lo] (row stride vstride).  Read y (d floats) + gather T,
 // write V: the sampling runs at full occupancy with no Gram registers or barriers.
-template <int D, bool POW2, int SPT>
-__global__ void __launch_bounds__(256, 8) k_sample_v(const Args a, float* __restrict__ V, long long vstride) {
+// GV: also write grad T_k(y_k(p)) (interpolant gradient / spacing, zero outside the hull; the
+// values pass 2 would re-gather) as G[(k D + c) vstride + p], so pass 2 becomes a pure stream.
+template <int D, bool POW2, int SPT, bool GV>
+__global__ void __launch_bounds__(256, 8) k_sample_v(const Args a, float* __restrict__ V, float* __restrict__ G,
+                                                     long long vstride) {
   // grid (pixel blocks, K): block-uniform 64-bit bases, 32-bit per-thread offsets
   constexpr int BP = 256 * SPT;  // pixels per block
   const int npix = (int)(a.pix_hi - a.pix_lo);
@@ -281,29 +284,98 @@ __global__ void __launch_bounds__(256, 8) k_sample_v(const Args a, float* __rest
   float* vb = V + (long long)k * vstride + b0;
   const int nb = npix - b0;  // pixels left from this block's start
   const bool full = nb >= BP;
+  // GV: y is read once (evict first); V and grad T are re-read by the Gram and the streaming pass 2
+  // (evict last), so they should survive in L2 until then
+  const uint64_t pol_first = GV ? l2_policy_evict_first() : 0, pol_last = GV ? l2_policy_evict_last() : 0;
   float p[SPT][D];
 #pragma unroll
   for (int e = 0; e < SPT; ++e) {
     const int pe = full ? tid + 256 * e : min(tid + 256 * e, nb - 1);
 #pragma unroll
-    for (int c = 0; c < D; ++c) p[e][c] = __ldg(yb + (long long)c * a.y_stride + pe);
+    for (int c = 0; c < D; ++c)
+      p[e][c] = GV ? ldg_hint(yb + (long long)c * a.y_stride + pe, pol_first) : __ldg(yb + (long long)c * a.y_stride + pe);
   }
-  float v[SPT];
+  float v[SPT], gd[SPT][D];
 #pragma unroll
-  for (int e = 0; e < SPT; ++e) {
-    float gd[D];
-    v[e] = interp<float, float, D, false, POW2>(img, a.g, p[e], gd);
-  }
+  for (int e = 0; e < SPT; ++e) v[e] = interp<float, float, D, GV, POW2>(img, a.g, p[e], gd[e]);
   const float* shifts = reinterpret_cast<const float*>(a.shifts);
   const float sh = shifts ? shifts[fi] : 0.f;
-  if (full) {
+  float* gb = GV ? G + (long long)(k * D) * vstride + b0 : nullptr;
 #pragma unroll
-    for (int e = 0; e < SPT; ++e) vb[tid + 256 * e] = v[e] - sh;
-  } else {
+  for (int e = 0; e < SPT; ++e) {
+    const int pe = tid + 256 * e;
+    if (full || pe < nb) {
+      if (GV) {
+        stg_hint(vb + pe, v[e] - sh, pol_last);
 #pragma unroll
-    for (int e = 0; e < SPT; ++e)
-      if (tid + 256 * e < nb) vb[tid + 256 * e] = v[e] - sh;
+        for (int c = 0; c < D; ++c) stg_hint(gb + (long long)c * vstride + pe, gd[e][c], pol_last);
+      } else {
+        vb[pe] = v[e] - sh;
+      }
+    }
   }
+}
+
+// Streaming pass 2 (fp32 NCC displacement, K <= 32) after a k_sample_v<GV = true> pass 1 on the same
+// y: block = 64 pixels x 4 frame groups; thread (pixel, group g) forms q_j = beta'_j + sum_i M'_ij V_i(p)
+// for the 8 frames j = 8 g .. 8 g + 7 (V read by the 4 group threads: L1 hits; M' broadcast from
+// shared memory) and writes dD/dy_j,c(p) = q_j G_j,c(p).  No gathers and no y: V, G in, dD/dy out.
+template <int D>
+__global__ void __launch_bounds__(256) k_pass2_stream(const Args a, const float* __restrict__ V,
+                                                      const float* __restrict__ G, long long vstride) {
+  constexpr int KP = 32, PB = 64, JG = 8;
+  __shared__ __align__(16) float Ms[KP * KP];  // Ms[i][j], zero past K
+  __shared__ float bs[KP];
+  const int tid = threadIdx.x;
+  const int K = a.K;
+  const StatsLayout L(K);
+  const float* Mg = coef_ptr<float>(a.stats, L);
+  for (int e = tid; e < KP * KP; e += 256) {
+    const int i = e / KP, j = e % KP;
+    Ms[e] = (i < K && j < K) ? Mg[i * K + j] : 0.f;
+  }
+  if (tid < KP) bs[tid] = tid < K ? (float)a.stats[L.beta + tid] : 0.f;
+  __syncthreads();
+  const int g = tid / PB, px = tid % PB;  // warps 0-1: group 0, ... (lanes on consecutive pixels)
+  const int j0 = g * JG;
+  if (j0 >= K) return;
+  const long long npix = a.pix_hi - a.pix_lo;
+  const long long pl = (long long)blockIdx.x * PB + px;
+  if (pl >= npix) return;
+  const float* __restrict__ vp = V + pl;
+  const uint64_t pol = l2_policy_evict_first();  // last use of V / grad T; dD/dy is streamed out
+  float v[KP];
+#pragma unroll
+  for (int i = 0; i < KP; ++i) v[i] = i < K ? __ldg(vp + (long long)i * vstride) : 0.f;
+  float q[JG];
+#pragma unroll
+  for (int jj = 0; jj < JG; ++jj) q[jj] = bs[j0 + jj];
+#pragma unroll
+  for (int i = 0; i < KP; ++i) {
+    const float4 m0 = *reinterpret_cast<const float4*>(Ms + i * KP + j0);
+    const float4 m1 = *reinterpret_cast<const float4*>(Ms + i * KP + j0 + 4);
+    q[0] = fmaf(m0.x, v[i], q[0]);
+    q[1] = fmaf(m0.y, v[i], q[1]);
+    q[2] = fmaf(m0.z, v[i], q[2]);
+    q[3] = fmaf(m0.w, v[i], q[3]);
+    q[4] = fmaf(m1.x, v[i], q[4]);
+    q[5] = fmaf(m1.y, v[i], q[5]);
+    q[6] = fmaf(m1.z, v[i], q[6]);
+    q[7] = fmaf(m1.w, v[i], q[7]);
+  }
+  float* __restrict__ ob = reinterpret_cast<float*>(a.out) + (a.pix_lo - a.o_off) + pl;
+  const float* __restrict__ gp = G + pl;
+  float gv[JG][D];
+#pragma unroll
+  for (int jj = 0; jj < JG; ++jj)
+#pragma unroll
+    for (int c = 0; c < D; ++c)
+      gv[jj][c] = j0 + jj < K ? ldg_hint(gp + (long long)((j0 + jj) * D + c) * vstride, pol) : 0.f;
+#pragma unroll
+  for (int jj = 0; jj < JG; ++jj)
+    if (j0 + jj < K)
+#pragma unroll
+      for (int c = 0; c < D; ++c) stg_hint(ob + (long long)((j0 + jj) * D + c) * a.o_stride, q[jj] * gv[jj][c], pol);
 }
 
 // Split pass 1, kernel B: the K x K raw Gram of V on the tensor cores.  mbarrier pipeline,

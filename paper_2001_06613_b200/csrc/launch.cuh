@@ -242,15 +242,20 @@ cudaError_t run_curvature(const Launch& L, const Args& a, double alpha, double h
 // Split pass 1 for fp32 NCC displacement (K <= 32): k_sample_v (V = v - shift, [K][vstride])
 // then k_gram_tc (TMA V tiles -> hi/lo SW128 tiles -> tcgen05 Gram).  engine_tc.cuh.
 template <int D>
-cudaError_t run_pass1_split(const Launch& L, const Args& a, float* V, long long vstride, double* part,
+cudaError_t run_pass1_split(const Launch& L, const Args& a, float* V, float* G, long long vstride, double* part,
                             size_t part_cap, int* nblk) {
   const long long npix = a.pix_hi - a.pix_lo;
   if (npix <= 0) return cudaErrorInvalidValue;
   constexpr int SPT = 4;
   const long long per_frame = (npix + 256 * SPT - 1) / (256 * SPT);
   const dim3 sgrid((unsigned)per_frame, (unsigned)a.K);
-  if (a.g.pow2) k_sample_v<D, true, SPT><<<sgrid, 256, 0, L.stream>>>(a, V, vstride);
-  else k_sample_v<D, false, SPT><<<sgrid, 256, 0, L.stream>>>(a, V, vstride);
+  if (G) {
+    if (a.g.pow2) k_sample_v<D, true, SPT, true><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
+    else k_sample_v<D, false, SPT, true><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
+  } else {
+    if (a.g.pow2) k_sample_v<D, true, SPT, false><<<sgrid, 256, 0, L.stream>>>(a, V, nullptr, vstride);
+    else k_sample_v<D, false, SPT, false><<<sgrid, 256, 0, L.stream>>>(a, V, nullptr, vstride);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   EncodeTiledFn fn = encode_tiled_fn();
@@ -279,10 +284,19 @@ cudaError_t run_pass1_split(const Launch& L, const Args& a, float* V, long long 
   *nblk = grid;
   return cudaGetLastError();
 }
-cudaError_t pass1_split_d2(const Launch& L, const Args& a, float* V, long long vstride, double* part, size_t cap,
-                           int* nblk);
-cudaError_t pass1_split_d3(const Launch& L, const Args& a, float* V, long long vstride, double* part, size_t cap,
-                           int* nblk);
+cudaError_t pass1_split_d2(const Launch& L, const Args& a, float* V, float* G, long long vstride, double* part,
+                           size_t cap, int* nblk);
+cudaError_t pass1_split_d3(const Launch& L, const Args& a, float* V, float* G, long long vstride, double* part,
+                           size_t cap, int* nblk);
+template <int D>
+cudaError_t run_pass2_stream(const Launch& L, const Args& a, const float* V, const float* G, long long vstride) {
+  const long long npix = a.pix_hi - a.pix_lo;
+  if (npix <= 0) return cudaSuccess;
+  k_pass2_stream<D><<<(unsigned)((npix + 63) / 64), 256, 0, L.stream>>>(a, V, G, vstride);
+  return cudaGetLastError();
+}
+cudaError_t pass2_stream_d2(const Launch& L, const Args& a, const float* V, const float* G, long long vstride);
+cudaError_t pass2_stream_d3(const Launch& L, const Args& a, const float* V, const float* G, long long vstride);
 
 // Dispatch over (FEAT, PARAM, KP) for fixed (T, D).
 template <typename T, int D>

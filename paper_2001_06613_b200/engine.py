@@ -115,6 +115,10 @@ class Engine:
     def set_grid_ctas(self, ctas: int) -> None:
         check(self.lib.sr_set_grid_ctas(self.ctx, int(ctas)))
 
+    def set_sample_reuse(self, enable: bool) -> None:
+        """sr_grad may reuse the samples of the preceding sr_corr_partial (y unchanged in between)."""
+        check(self.lib.sr_set_sample_reuse(self.ctx, 1 if enable else 0))
+
     # ------------------------------------------------------------------ frames
     def frames_for(self, seq, dtype: torch.dtype, cache_size: int = 8) -> "DeviceFrames":
         """Upload (once) and cache the frames of a reference ImageSequence."""

@@ -133,8 +133,17 @@ class ShardedFieldObjective:
         raw = self.plan.corr_partial(prob)
         allreduce_raw(raw, self.k, self.group)
         self.plan.finalize(prob, self.weights, self.cell_volume, n_total=self.grid.cell_count)
-        self.plan.grad(prob, grad_local, g_off=self.lo)
+        self._grad(prob, grad_local)
         return self.plan.stats
+
+    def _grad(self, prob, grad_local):
+        """Pass 2 on the samples cached by this evaluation's pass 1 (y is unchanged in between)."""
+        eng = self.frames.engine
+        eng.set_sample_reuse(True)
+        try:
+            self.plan.grad(prob, grad_local, g_off=self.lo)
+        finally:
+            eng.set_sample_reuse(False)
 
     def kernel_times(self, y_local, grad_local, flush: torch.Tensor | None = None, reps: int = 20) -> dict:
         """Mean CUDA-event time (ms) of pass 1 (+ its CTA reduce), finalize (+ all-reduce when
@@ -152,7 +161,7 @@ class ShardedFieldObjective:
             allreduce_raw(raw, self.k, self.group)
             self.plan.finalize(prob, self.weights, self.cell_volume, n_total=self.grid.cell_count)
             ev[2].record(stream)
-            self.plan.grad(prob, grad_local, g_off=self.lo)
+            self._grad(prob, grad_local)
             ev[3].record(stream)
             torch.cuda.synchronize()
             acc["pass1"] += ev[0].elapsed_time(ev[1])
