@@ -612,7 +612,6 @@ __device__ void finalize_block(const double* __restrict__ raw, const Job* job, i
     double cp = 0.0, dp = 0.0;
     for (int i = lane; i < K; i += 32) {
       const double c = Cmat[i * K + j];
-      stats[L.C + i * K + j] = c;
       const double wc2 = w[i] * c * c;
       cp += wc2;
       if (i != j) dp += wc2 * w[j];
@@ -625,8 +624,10 @@ __device__ void finalize_block(const double* __restrict__ raw, const Job* job, i
     }
   }
   __syncthreads();
+  for (int e = tid; e < K * K; e += nt) stats[L.C + e] = Cmat[e];  // coalesced
+  __syncthreads();
   // M'_ij = -4 h w_j (w_i C_ij / sig_i - delta_ij c_j / sig_j) / sig_j ;  beta'_j = -sum_i M'_ij mu_i
-  float* Mf = reinterpret_cast<float*>(stats + L.Mf);
+  // (M' overwrites C in shared memory: each element is read and written by the same thread)
   for (int j = warp; j < K; j += nw) {
     double bp = 0.0;
     for (int i = lane; i < K; i += 32) {
@@ -636,12 +637,18 @@ __device__ void finalize_block(const double* __restrict__ raw, const Job* job, i
         if (i == j) t -= cj[j] * isg[j];
         m = -4.0 * h * w[j] * t * isg[j];
       }
-      stats[L.M + i * K + j] = m;
-      Mf[i * K + j] = (float)m;
+      Cmat[i * K + j] = m;
       bp += m * mu[i];
     }
     bp = warp_sum(bp);
     if (lane == 0) stats[L.beta + j] = feat == NCC ? -bp : 0.0;
+  }
+  __syncthreads();
+  float* Mf = reinterpret_cast<float*>(stats + L.Mf);
+  for (int e = tid; e < K * K; e += nt) {  // coalesced
+    const double m = Cmat[e];
+    stats[L.M + e] = m;
+    Mf[e] = (float)m;
   }
   if (warp == 0) {
     double dsum = 0.0, sw = 0.0, sw2 = 0.0;

@@ -388,7 +388,8 @@ __global__ void __launch_bounds__(256) k_pass2_stream(const Args a, const float*
 // The flush lags the MMAs by up to NA tiles, so it never stalls the splitters.
 struct TCG {
   static constexpr int NSP = 512, NT = NSP + 32 + 128;  // splitters, issuer warp, flushers
-  static constexpr int KP = 32, TP = 128, NST = 6, NB = 3, NA = 4, NACC = 4;  // NACC chains per tile
+  static constexpr int KP = 32, TP = 128, NST = 6, NB = 3, NA = 4, NACC = 1;  // NACC chains per tile
+  static constexpr int R = 2;  // tiles accumulated in one TMEM slot (fp32) between fp64 flushes
   static constexpr int VBYTES = 64 * TP * 4, SBYTES = KP * TP * 4;
   static constexpr uint32_t IDESC = umma_idesc_tf32(64, 32);
 };
@@ -520,21 +521,22 @@ static __global__ void __launch_bounds__(TCG::NT, 1) k_gram_tc(const Args a, con
     if (lane == 0) {
       for (long long n = 0; n < nloc && n < NST; ++n) load_tile(n, (int)n);
       for (long long n = 0; n < nloc; ++n) {
-        const int b = (int)(n % NB), s = (int)(n % NA), st = (int)(n % NST);
+        const long long grp = n / C::R;  // accumulation group: R consecutive tiles share a TMEM slot
+        const bool first = n % C::R == 0, last = n % C::R == C::R - 1 || n == nloc - 1;
+        const int b = (int)(n % NB), s = (int)(grp % NA), st = (int)(n % NST);
         mbar_wait(&vb_full[b], (uint32_t)((n / NB) & 1));
         if (n + NST < nloc) load_tile(n + NST, st);  // every splitter has read stage st: refill it
-        if (n >= NA) mbar_wait(&acc_free[s], (uint32_t)((n / NA - 1) & 1));
+        if (first && grp >= NA) mbar_wait(&acc_free[s], (uint32_t)((grp / NA - 1) & 1));
         tc_fence_after();
         const uint32_t vaddr = smem_u32(Vb + (size_t)b * C::VBYTES);
 #pragma unroll
         for (int k8 = 0; k8 < TP / 8; ++k8) {
-          if (a.dbg & 64) break;
           const uint64_t d = umma_sdesc_sw128(vaddr + (uint32_t)((k8 >> 2) * 8192 + (k8 & 3) * 32));
           umma_tf32(tmem + (uint32_t)((s * C::NACC + k8 % C::NACC) * 32), d, d, C::IDESC,
-                    k8 >= C::NACC ? 1u : 0u);
+                    (k8 >= C::NACC || !first) ? 1u : 0u);
         }
         umma_commit(&vb_free[b]);
-        umma_commit(&acc_full[s]);
+        if (last) umma_commit(&acc_full[s]);
       }
     }
     __syncwarp();
@@ -542,7 +544,8 @@ static __global__ void __launch_bounds__(TCG::NT, 1) k_gram_tc(const Args a, con
     // =============================== flushers: TMEM lane quarter q = warp % 4 holds rows 16q..16q+15
     const int q = warp & 3, mrow = 16 * q + lane;
     double* acc = accs + mrow * 33;
-    for (long long n = 0; n < nloc; ++n) {
+    const long long ngrp = (nloc + C::R - 1) / C::R;
+    for (long long n = 0; n < ngrp; ++n) {
       const int s = (int)(n % NA);
       mbar_wait(&acc_full[s], (uint32_t)((n / NA) & 1));
       tc_fence_after();
