@@ -81,20 +81,31 @@ class FieldObjective:
     def host_stats(self) -> dict:
         return self.plan.host_stats()
 
-    def evaluate_host(self, y_host: np.ndarray):
-        """End-to-end evaluation from host memory: (J, dJ/dy) as (float, ndarray)."""
+    def evaluate_host(self, y_host):
+        """End-to-end evaluation from host memory: (J, dJ/dy) as (float, ndarray).
+
+        ``y_host`` may be a numpy array (staged through an internal pinned buffer) or a pinned CPU
+        ``torch.Tensor`` of the field's shape and dtype, which is copied to the device directly (the
+        e2e contract: inputs already in pinned host memory).  The returned gradient is a view of an
+        internal pinned buffer, overwritten by the next call."""
         shape = self.shape
-        y_host = np.asarray(y_host)
-        if y_host.shape != shape:
-            raise ValueError(f"y must have shape {shape}")
         dt = self.frames.dtype
         if self._pinned_y is None:
             self._pinned_y = torch.empty(shape, dtype=dt, pin_memory=True)
             self._pinned_g = torch.empty(shape, dtype=dt, pin_memory=True)
             self._dev_y = torch.empty(shape, dtype=dt, device=self.frames.data.device)
             self._dev_g = torch.empty(shape, dtype=dt, device=self.frames.data.device)
-        self._pinned_y.numpy()[...] = y_host
-        self._dev_y.copy_(self._pinned_y, non_blocking=True)
+        if isinstance(y_host, torch.Tensor) and y_host.device.type == "cpu" and y_host.is_pinned():
+            if tuple(y_host.shape) != tuple(shape) or y_host.dtype != dt:
+                raise ValueError(f"y must have shape {shape} and dtype {dt}")
+            src = y_host.contiguous()
+        else:
+            y_host = np.asarray(y_host)
+            if y_host.shape != shape:
+                raise ValueError(f"y must have shape {shape}")
+            self._pinned_y.numpy()[...] = y_host
+            src = self._pinned_y
+        self._dev_y.copy_(src, non_blocking=True)
         stats, g = self.evaluate(self._dev_y, self._dev_g)
         self._pinned_g.copy_(g, non_blocking=True)
         d = stats[0:1].to("cpu", non_blocking=False)
