@@ -50,6 +50,8 @@ struct sr_ctx {
   size_t vbuf_bytes = 0;
   float* gbuf = nullptr;  // split pass 1 with the streaming pass 2: grad T, [K][d][vstride]
   size_t gbuf_bytes = 0;
+  float* ngfbuf = nullptr;  // split NGF path: u, grad T, n, rho, z in one allocation
+  size_t ngfbuf_bytes = 0;
   int p2s = 1;            // SEQREG_B200_P2S=0: re-gathering pass 2 instead of the streaming pass 2
   int sample_reuse = 0;   // sr_set_sample_reuse: sr_grad may reuse the samples of the last sr_corr_partial
   // what vbuf / gbuf hold: the samples of this (y, slab, frames, subset); pass 2 reuses them on a match
@@ -59,6 +61,8 @@ struct sr_ctx {
     const void* frames = nullptr;
     const void* shifts = nullptr;
     int64_t y_off = 0, y_stride = 0, pix_lo = 0, pix_hi = 0, vstride = 0;
+    int feature = 0;
+    sr::NgfBufs ngf{};  // the split NGF path's buffers and ranges (feature == SR_NGF)
     int frame_index[SR_MAX_FRAMES];
   } vtag;
   Job* job_dev = nullptr;
@@ -281,10 +285,17 @@ static cudaError_t launch_reduce_finalize(sr_ctx* c, const sr_problem* p, int nb
 // pass 1 over the slab, then the fixed-order cross-CTA reduction into raw (and, with
 // stats != nullptr, the finalize in the same launch)
 // KP of the pass-1 partial layout: the tcgen05 kernel always uses 32 (frames padded)
+// the split NGF path: fp32 displacement fields, K <= 128, tensor-core Gram (KP = 128 partials)
+static bool ngf_split(const sr_ctx* c, const sr_problem* p) {
+  return p->dtype == SR_F32 && p->feature == SR_NGF && p->param == SR_DISPLACEMENT && p->k <= 128 && !c->legacy &&
+         c->tc && c->split;
+}
+
 static int pass1_kp(const sr_ctx* c, const sr_problem* p) {
   if (p->dtype == SR_F32 && p->feature == SR_NCC && p->param == SR_DISPLACEMENT && p->k <= 32 && !c->legacy &&
       c->tc)
     return 32;
+  if (ngf_split(c, p)) return p->k <= 64 ? 64 : 128;
   return kp_of(p->k);
 }
 
@@ -302,6 +313,7 @@ static void set_vtag(sr_ctx* c, const sr_problem* p, long long vstride, int has_
   t.pix_lo = p->pix_lo;
   t.pix_hi = p->pix_hi;
   t.vstride = vstride;
+  t.feature = p->feature;
   for (int k = 0; k < p->k; ++k) t.frame_index[k] = p->frame_index[k];
 }
 
@@ -309,7 +321,7 @@ static void set_vtag(sr_ctx* c, const sr_problem* p, long long vstride, int has_
 // (the caller's contract: sr_grad follows the sr_corr_* calls at the same y)
 static bool vtag_matches(const sr_ctx* c, const sr_problem* p) {
   const sr_ctx::VTag& t = c->vtag;
-  if (!t.valid || !t.has_g || t.k != p->k || t.ndim != p->grid.ndim || t.y != p->y_dev ||
+  if (!t.valid || !t.has_g || t.feature != p->feature || t.k != p->k || t.ndim != p->grid.ndim || t.y != p->y_dev ||
       t.frames != p->frames_dev || t.shifts != p->shifts_dev || t.y_off != p->y_off || t.y_stride != p->y_stride ||
       t.pix_lo != p->pix_lo || t.pix_hi != p->pix_hi)
     return false;
@@ -329,8 +341,41 @@ static int corr_partial_impl(sr_ctx* c, const sr_problem* p, double* raw, double
   const Launch L = launch_of(c);
   int nblk = 0;
   const long long npix = p->pix_hi - p->pix_lo;
-  if (KP == 32 && p->dtype == SR_F32 && p->feature == SR_NCC && p->param == SR_DISPLACEMENT && c->split && c->tc &&
-      !c->legacy && npix > 0) {
+  if ((KP == 64 || KP == 128) && ngf_split(c, p) && npix > 0) {
+    const Geo g = a.g;
+    const long long row = g.st[g.nd - 1];
+    sr::NgfBufs B{};
+    B.vlo = std::max<long long>(0, p->pix_lo - 2 * row);
+    B.vhi = std::min<long long>(g.N, p->pix_hi + 2 * row);
+    B.zlo = std::max<long long>(0, p->pix_lo - row);
+    B.zhi = std::min<long long>(g.N, p->pix_hi + row);
+    B.vstride = (B.vhi - B.vlo + 3) & ~3LL;
+    B.zstride = (B.zhi - B.zlo + 3) & ~3LL;
+    const int d = g.nd;
+    const size_t nv = (size_t)p->k * B.vstride, nz = (size_t)p->k * B.zstride;
+    const size_t total = nv * (1 + d) + nz * (2 * d + 1);  // u, grad T | n, z, rho
+    void* nb = c->ngfbuf;
+    rc = ensure(&nb, &c->ngfbuf_bytes, total * 4);
+    if (rc) return rc;
+    c->ngfbuf = (float*)nb;
+    B.V = c->ngfbuf;
+    B.G = B.V + nv;
+    B.Nf = B.G + nv * d;
+    B.Z = B.Nf + nz * d;
+    B.Rho = B.Z + nz * d;
+    c->vtag.valid = 0;
+    const cudaError_t e1 = d == 2 ? ngf_pass1_d2(L, a, B, c->part, c->part_cap, &nblk)
+                                  : ngf_pass1_d3(L, a, B, c->part, c->part_cap, &nblk);
+    if (e1 == cudaSuccess) {
+      set_vtag(c, p, B.vstride, 1);
+      c->vtag.ngf = B;
+    } else if (e1 != cudaErrorNotSupported) {
+      CK(e1);
+    } else {  // layout the tensor map cannot express: the generic kernels with the same KP layout
+      CK(SR_SWITCH(p->dtype, p->grid.ndim, pass1, p->feature, p->param, KP, L, a, c->part, c->part_cap, &nblk));
+    }
+  } else if (KP == 32 && p->dtype == SR_F32 && p->feature == SR_NCC && p->param == SR_DISPLACEMENT && c->split &&
+             c->tc && !c->legacy && npix > 0) {
     const long long vstride = (npix + 3) & ~3LL;  // V = v - shift, [K][vstride]
     void* vb = c->vbuf;
     rc = ensure(&vb, &c->vbuf_bytes, (size_t)p->k * vstride * 4);
@@ -464,6 +509,7 @@ int sr_destroy(sr_ctx* c) {
   sr::lbfgs::destroy(c->lbfgs);
   cudaFree(c->vbuf);
   cudaFree(c->gbuf);
+  cudaFree(c->ngfbuf);
   for (auto& t : c->texsets) texset_free(t);
   cudaFree(c->zbuf);
   cudaFree(c->aux);
@@ -629,6 +675,13 @@ static int grad_impl(sr_ctx* c, const sr_problem* p, const double* stats, void* 
       k_affine_rows<<<(warps * 32 + 255) / 256, 256, 0, c->stream>>>(c->aux, nblk, KP, p->k, na, 0, (double*)grad);
       CK(cudaGetLastError());
     }
+    return SR_OK;
+  }
+  if (reuse && ngf_split(c, p) && vtag_matches(c, p)) {  // split NGF pass 2: no re-sampling
+    a.out = grad;
+    a.o_off = g_off;
+    a.o_stride = g_stride;
+    CK(d == 2 ? ngf_pass2_d2(L, a, c->vtag.ngf) : ngf_pass2_d3(L, a, c->vtag.ngf));
     return SR_OK;
   }
   // NGF: z over the slab extended by one slowest-axis row on each side (the adjoint stencil)

@@ -1245,3 +1245,4 @@ __global__ void __launch_bounds__(1024) k_frame_mean(const T* __restrict__ frame
 
 #include "engine_ws.cuh"
 #include "engine_tc.cuh"
+#include "engine_ngf.cuh"

@@ -1,0 +1,340 @@
+// engine_ngf.cuh — split NGF path (fp32, displacement fields, K <= 128): no neighbour re-sampling,
+// tensor-core Gram, streaming pass 2.  DESIGN.md §4.
+//
+//   k_sample_v (engine_tc.cuh, no shift)  u = T_k(y_k) and grad T_k over the slab +- 2 rows
+//   k_ngf_feat                             n = grad_h u / rho, rho = sqrt(|grad_h u|^2 + eps^2)
+//                                          (the stencil of ngf_at, engine.cuh) over the slab +- 1 row
+//   k_gram_tcx<64|128>                     raw Gram  sum_(p, c) n_i n_j  over the slab on tcgen05 (3xTF32)
+//   k_ngf_z                                r = M'^T n (per pixel and component), z = (r - n (n.r)) / rho
+//   k_ngf_adj_stream                       dD/dy = (D_h^T z) grad T
+#pragma once
+
+namespace sr {
+
+__device__ __forceinline__ void coords_flat(const Geo& g, int p, int (&c)[3]) {
+  c[0] = p % g.n[0];
+  c[1] = g.nd > 1 ? (p / g.n[0]) % g.n[1] : 0;
+  c[2] = g.nd > 2 ? p / (g.n[0] * g.n[1]) : 0;
+}
+
+// n, rho at pixels [zlo, zhi) of every subset frame from u = V[k][p - vlo] (same float arithmetic
+// as ngf_at: central differences inside, one-sided at the domain edge, world units)
+template <int D>
+__global__ void __launch_bounds__(256) k_ngf_feat(const Args a, const float* __restrict__ V, long long vlo,
+                                                  long long vstride, float* __restrict__ Nf, float* __restrict__ Rho,
+                                                  long long zlo, long long zhi, long long zstride) {
+  const int k = blockIdx.y;
+  const long long p = zlo + (long long)blockIdx.x * 256 + threadIdx.x;
+  if (p >= zhi) return;
+  int c[3];
+  coords_flat(a.g, (int)p, c);
+  const float* u = V + (long long)k * vstride - vlo;
+  float g[D];
+  float pn = 0.f;
+#pragma unroll
+  for (int ax = 0; ax < D; ++ax) {
+    const bool hp = c[ax] < a.g.n[ax] - 1, hm = c[ax] > 0;
+    const long long st = a.g.sti[ax];
+    const float up = __ldg(u + (hp ? p + st : p)), um = __ldg(u + (hm ? p - st : p));
+    const float inv = (float)a.g.inv[ax];
+    g[ax] = (hp && hm) ? (up - um) * (inv * 0.5f) : (up - um) * inv;
+    pn += g[ax] * g[ax];
+  }
+  const float e = (float)a.eps;
+  const float rho = sqrtf(pn + e * e);
+  const float ir = 1.f / rho;
+#pragma unroll
+  for (int ax = 0; ax < D; ++ax) Nf[((long long)k * D + ax) * zstride + (p - zlo)] = g[ax] * ir;
+  Rho[(long long)k * zstride + (p - zlo)] = rho;
+}
+
+// ------------------------------------------------------------------------------------------
+// Raw NGF Gram G_ij = sum over the slab's pixels and components of n_i n_j, for up to 128 frames.
+// Tiles of 32 columns of one component ([128 frames x 32] TMA box of a 3-D map over
+// Nf [K][D][zstride], zero fill past K and past the slab); 16 splitter warps turn a tile into
+// hi/lo tf32 halves (SWIZZLE_128B, K-major) and keep max |n| per frame; one lane issues per K8
+// step three M128 N128 K8 MMAs (hi.hi^T, lo.hi^T, hi.lo^T) into one TMEM slot (R tiles per slot,
+// ring of NA slots); 4 flusher warps add the slot into fp64 accumulators in shared memory, whose
+// column index is XOR-swizzled by the row (conflict-free for a lane-per-row flush).
+// KP = 128: hi (128 rows) and lo operands; per K8 step three M128 N128 MMAs (hi.hi^T + lo.hi^T +
+// hi.lo^T) give G directly.  KP = 64: one 128-row operand [hi (64 rows); lo (64 rows)] and one
+// M128 N64 MMA per K8 step (B = the hi rows) give HH (rows 0-63) and LH (rows 64-127);
+// G = HH + LH + LH^T at the end.
+template <int KP_>
+struct TGX {
+  static constexpr int KP = KP_;
+  static constexpr int NSP = 512, NT = NSP + 32 + 128;
+  static constexpr int TP = KP == 64 ? 64 : 32;  // columns per tile (shared-memory bound at KP = 128)
+  static constexpr int NST = 2, NB = 2, NA = 2, R = 4;
+  static constexpr int N = KP;                   // MMA N and TMEM columns per slot
+  static constexpr int SBYTES = KP * TP * 4;     // fp32 stage [KP][32]
+  static constexpr int OBYTES = 128 * TP * 4;    // one 128-row operand tile (TP / 32 column atoms of 16 KB)
+  static constexpr int NOPS = KP == 128 ? 2 : 1; // operand tiles per buffer (hi, lo) or ([hi; lo])
+  static constexpr uint32_t IDESC = umma_idesc_tf32(128, N);
+  static constexpr int ACC_ROWS = 128, ACC_COLS = N;
+};
+
+template <int KP>
+constexpr size_t tgx_smem() {
+  using C = TGX<KP>;
+  return 1024 + (size_t)C::NST * C::SBYTES + (size_t)C::NB * C::NOPS * C::OBYTES +
+         (size_t)C::ACC_ROWS * C::ACC_COLS * 8 + 512;
+}
+
+template <int KP>
+__global__ void __launch_bounds__(TGX<KP>::NT, 1) k_gram_tcx(const Args a, const __grid_constant__ CUtensorMap xmap,
+                                                            int ntx, int ncomp) {
+  using C = TGX<KP>;
+  constexpr int TP = C::TP, NST = C::NST, NB = C::NB, NA = C::NA, NC = C::ACC_COLS;
+  extern __shared__ __align__(1024) unsigned char smem_gx[];
+  unsigned char* base = smem_gx + ((1024 - (smem_u32(smem_gx) & 1023)) & 1023);
+  float* stage = reinterpret_cast<float*>(base);                                       // [NST][KP][32]
+  unsigned char* Vb = base + (size_t)NST * C::SBYTES;                                  // [NB][NOPS][128 x 32]
+  double* accs = reinterpret_cast<double*>(Vb + (size_t)NB * C::NOPS * C::OBYTES);     // [128][NC] swizzled
+  uint64_t* bars = reinterpret_cast<uint64_t*>(accs + C::ACC_ROWS * NC);
+  uint64_t* st_full = bars;
+  uint64_t* vb_full = st_full + NST;
+  uint64_t* vb_free = vb_full + NB;
+  uint64_t* acc_full = vb_free + NB;
+  uint64_t* acc_free = acc_full + NA;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_free + NA);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int K = a.K;
+  const long long ntiles = (long long)ntx * ncomp;
+  const long long nloc = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  auto load_tile = [&](long long n, int st) {
+    const long long t = blockIdx.x + n * gridDim.x;
+    mbar_arrive_expect_tx(&st_full[st], (uint32_t)C::SBYTES);
+    tma_load_3d(stage + (size_t)st * KP * TP, &xmap, (int)(t % ntx) * TP, (int)(t / ntx), 0, &st_full[st]);
+  };
+  if (tid == 0) {
+    for (int s = 0; s < NST; ++s) mbar_init(&st_full[s], 1);
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(&vb_full[b], C::NSP);
+      mbar_init(&vb_free[b], 1);
+    }
+    for (int s = 0; s < NA; ++s) {
+      mbar_init(&acc_full[s], 1);
+      mbar_init(&acc_free[s], 128);
+    }
+    fence_mbar_init();
+    tma_prefetch_desc(&xmap);
+  }
+  for (int e = tid; e < C::ACC_ROWS * NC; e += C::NT) accs[e] = 0.0;
+  if (warp == C::NSP / 32) tmem_alloc(tmem_slot, NC * NA);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  double* out = a.part + (size_t)blockIdx.x * (KP * KP + 3 * KP);
+
+  if (tid < C::NSP) {
+    // ======================= splitters: KP = 128: row r = tid / 4, 8 columns; KP = 64: row tid / 8, 4 columns
+    constexpr int TPR = C::NSP / KP;  // threads per row
+    constexpr int CPT = TP / TPR;     // columns per thread (8 or 4)
+    const int r = tid / TPR, part = tid % TPR;
+    float fmx = 0.f;
+    for (long long n = 0; n < nloc; ++n) {
+      const int b = (int)(n % NB), st = (int)(n % NST);
+      mbar_wait(&st_full[st], (uint32_t)((n / NST) & 1));
+      const float* src = stage + (size_t)st * KP * TP + (size_t)r * TP + part * CPT;
+      float4 qq[CPT / 4];
+#pragma unroll
+      for (int h = 0; h < CPT / 4; ++h) qq[h] = *reinterpret_cast<const float4*>(src + 4 * h);
+      if (n >= NB) mbar_wait(&vb_free[b], (uint32_t)((n / NB - 1) & 1));
+      unsigned char* ob = Vb + (size_t)b * C::NOPS * C::OBYTES;
+#pragma unroll
+      for (int h = 0; h < CPT / 4; ++h) {
+        const float qv[4] = {qq[h].x, qq[h].y, qq[h].z, qq[h].w};
+        float hi[4], lo[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          fmx = fmaxf(fmx, fabsf(qv[u]));
+          hi[u] = to_tf32(qv[u]);
+          lo[u] = qv[u] - hi[u];
+        }
+        const int col = part * CPT + 4 * h;
+        const int atom = col >> 5, g = (col & 31) >> 2;  // 128-row column atom (16 KB), 16-byte chunk
+        const int rh = r, rl = KP == 128 ? r : 64 + r;
+        unsigned char* hb = ob + atom * (128 * 128);
+        unsigned char* lb = (KP == 128 ? ob + C::OBYTES : ob) + atom * (128 * 128);
+        *reinterpret_cast<float4*>(hb + (rh >> 3) * 1024 + (rh & 7) * 128 + (((g ^ (rh & 7)) & 7) << 4)) =
+            make_float4(hi[0], hi[1], hi[2], hi[3]);
+        *reinterpret_cast<float4*>(lb + (rl >> 3) * 1024 + (rl & 7) * 128 + (((g ^ (rl & 7)) & 7) << 4)) =
+            make_float4(lo[0], lo[1], lo[2], lo[3]);
+      }
+      fence_proxy_async_smem();
+      mbar_arrive(&vb_full[b]);  // also releases stage st
+    }
+#pragma unroll
+    for (int o = 1; o < TPR; o <<= 1) fmx = fmaxf(fmx, __shfl_xor_sync(0xffffffffu, fmx, o));
+    if (part == 0) {
+      out[KP * KP + r] = 0.0;  // s: unused by NGF
+      out[KP * KP + KP + r] = r < K ? (double)fmx : 0.0;
+      out[KP * KP + 2 * KP + r] = r < K ? (double)fmx : 0.0;
+    }
+  } else if (warp == C::NSP / 32) {
+    // ======================= issuer
+    if (lane == 0) {
+      for (long long n = 0; n < nloc && n < NST; ++n) load_tile(n, (int)n);
+      for (long long n = 0; n < nloc; ++n) {
+        const long long grp = n / C::R;
+        const bool first = n % C::R == 0, last = n % C::R == C::R - 1 || n == nloc - 1;
+        const int b = (int)(n % NB), s = (int)(grp % NA), st = (int)(n % NST);
+        mbar_wait(&vb_full[b], (uint32_t)((n / NB) & 1));
+        if (n + NST < nloc) load_tile(n + NST, st);
+        if (first && grp >= NA) mbar_wait(&acc_free[s], (uint32_t)((grp / NA - 1) & 1));
+        tc_fence_after();
+        const uint32_t o0 = smem_u32(Vb + (size_t)b * C::NOPS * C::OBYTES);
+        const uint32_t acc = tmem + (uint32_t)(s * NC);
+#pragma unroll
+        for (int k8 = 0; k8 < TP / 8; ++k8) {
+          const uint32_t acc_in = (k8 > 0 || !first) ? 1u : 0u;
+          const uint32_t koff = (uint32_t)((k8 >> 2) * (128 * 128) + (k8 & 3) * 32);
+          const uint64_t dh = umma_sdesc_sw128(o0 + koff);
+          if (KP == 128) {
+            const uint64_t dl = umma_sdesc_sw128(o0 + C::OBYTES + koff);
+            umma_tf32(acc, dh, dh, C::IDESC, acc_in);
+            umma_tf32(acc, dl, dh, C::IDESC, 1u);
+            umma_tf32(acc, dh, dl, C::IDESC, 1u);
+          } else {
+            umma_tf32(acc, dh, dh, C::IDESC, acc_in);  // A = [hi; lo] (128 rows), B = hi (first 64 rows)
+          }
+        }
+        umma_commit(&vb_free[b]);
+        if (last) umma_commit(&acc_full[s]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ======================= flushers: TMEM lane quarter q = warp % 4, row m = 32 q + lane
+    const int q = warp & 3, m = 32 * q + lane;
+    double* arow = accs + (size_t)m * NC;
+    const long long ngrp = (nloc + C::R - 1) / C::R;
+    for (long long n = 0; n < ngrp; ++n) {
+      const int s = (int)(n % NA);
+      mbar_wait(&acc_full[s], (uint32_t)((n / NA) & 1));
+      tc_fence_after();
+#pragma unroll 1
+      for (int ch = 0; ch < NC / 32; ++ch) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(s * NC + ch * 32), v);
+#pragma unroll
+        for (int cc = 0; cc < 32; ++cc) arow[(32 * ch + cc) ^ lane] += (double)v[cc];
+      }
+      tc_fence_before();
+      mbar_arrive(&acc_free[s]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (tid >= C::NSP + 32) {
+    auto A = [&](int i, int j) { return accs[(size_t)i * NC + (j ^ (i & 31))]; };
+    for (int e = tid - (C::NSP + 32); e < KP * KP; e += 128) {
+      const int i = e / KP, j = e % KP;
+      out[e] = KP == 128 ? A(i, j) : A(i, j) + A(64 + i, j) + A(64 + j, i);
+    }
+  } else if (warp == C::NSP / 32) {
+    tc_fence_after();
+    tmem_dealloc(tmem, NC * NA);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// z over [zlo, zhi): block = ZP pixels x G groups of 16 frames.  The block's n tile [K][D][ZP] is
+// staged in shared memory once (coalesced); thread (pixel, group) forms r_(j,c) = sum_i M'_ij n_(i,c)
+// for its 16 frames (M' broadcast from shared memory), then z_(j,c) = (r_(j,c) - n_(j,c)
+// sum_c' n_(j,c') r_(j,c')) / rho_j.
+constexpr int NGF_ZP = 32, NGF_JG = 16;
+
+template <int D>
+__global__ void __launch_bounds__(256) k_ngf_z(const Args a, const float* __restrict__ Nf,
+                                               const float* __restrict__ Rho, long long zlo, long long zhi,
+                                               long long zstride, float* __restrict__ Z) {
+  constexpr int ZP = NGF_ZP, JG = NGF_JG;
+  extern __shared__ __align__(16) float sm_ngfz[];
+  const int K = a.K;
+  const int KP16 = (K + JG - 1) / JG * JG;
+  float* Ms = sm_ngfz;                        // [K][KP16], zero padded
+  float* Ns = Ms + (size_t)K * KP16;          // [K][D][ZP]
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const StatsLayout L(K);
+  const float* Mg = coef_ptr<float>(a.stats, L);
+  for (int e = tid; e < K * KP16; e += nt) {
+    const int i = e / KP16, j = e % KP16;
+    Ms[e] = j < K ? Mg[i * K + j] : 0.f;
+  }
+  const long long p0 = zlo + (long long)blockIdx.x * ZP;
+  for (int e = tid; e < K * D * ZP; e += nt) {
+    const int ic = e / ZP, px = e % ZP;
+    const long long p = p0 + px;
+    Ns[e] = p < zhi ? __ldg(Nf + (long long)ic * zstride + (p - zlo)) : 0.f;
+  }
+  __syncthreads();
+  const int px = tid % ZP, grp = tid / ZP, j0 = grp * JG;
+  const long long p = p0 + px;
+  if (j0 >= K || p >= zhi) return;
+  float r[JG][D];
+#pragma unroll
+  for (int jj = 0; jj < JG; ++jj)
+#pragma unroll
+    for (int c = 0; c < D; ++c) r[jj][c] = 0.f;
+#pragma unroll 2
+  for (int i = 0; i < K; ++i) {
+    float ni[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) ni[c] = Ns[(i * D + c) * ZP + px];
+    const float4* m4 = reinterpret_cast<const float4*>(Ms + i * KP16 + j0);
+#pragma unroll
+    for (int q = 0; q < JG / 4; ++q) {
+      const float4 m = m4[q];
+      const float mm[4] = {m.x, m.y, m.z, m.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int c = 0; c < D; ++c) r[4 * q + u][c] = fmaf(mm[u], ni[c], r[4 * q + u][c]);
+    }
+  }
+  const long long pz = p - zlo;
+#pragma unroll
+  for (int jj = 0; jj < JG; ++jj) {
+    const int j = j0 + jj;
+    if (j >= K) break;
+    float nj[D], dot = 0.f;
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      nj[c] = Ns[(j * D + c) * ZP + px];
+      dot += nj[c] * r[jj][c];
+    }
+    const float ir = 1.f / __ldg(Rho + (long long)j * zstride + pz);
+#pragma unroll
+    for (int c = 0; c < D; ++c) Z[((long long)j * D + c) * zstride + pz] = (r[jj][c] - nj[c] * dot) * ir;
+  }
+}
+
+// dD/dy_(k,c)(p) = (sum_ax D_h,ax^T z_(k,ax))(p) grad T_(k,c)(p) over the slab
+template <int D>
+__global__ void __launch_bounds__(256) k_ngf_adj_stream(const Args a, const float* __restrict__ Z, long long zlo,
+                                                        long long zstride, const float* __restrict__ Gv,
+                                                        long long vlo, long long vstride) {
+  const int k = blockIdx.y;
+  const long long p = a.pix_lo + (long long)blockIdx.x * 256 + threadIdx.x;
+  if (p >= a.pix_hi) return;
+  int c[3];
+  coords_flat(a.g, (int)p, c);
+  float du = 0.f;
+#pragma unroll
+  for (int ax = 0; ax < D; ++ax) {
+    const float* z = Z + ((long long)k * D + ax) * zstride;
+    du += dgrad_adjoint<float, D>(z, p - zlo, a.g.st[ax], c[ax], a.g.n[ax], (float)a.g.inv[ax]);
+  }
+  float* out = reinterpret_cast<float*>(a.out);
+#pragma unroll
+  for (int cc = 0; cc < D; ++cc)
+    out[((long long)k * D + cc) * a.o_stride + (p - a.o_off)] =
+        du * __ldg(Gv + ((long long)k * D + cc) * vstride + (p - vlo));
+}
+
+}  // namespace sr

@@ -284,6 +284,92 @@ cudaError_t run_pass1_split(const Launch& L, const Args& a, float* V, float* G, 
   *nblk = grid;
   return cudaGetLastError();
 }
+// Split NGF path (engine_ngf.cuh).  Ranges: V / grad T over [vlo, vhi) = slab +- 2 rows, n / rho / z over
+// [zlo, zhi) = slab +- 1 row, the Gram over the slab.  cudaErrorNotSupported: layouts the TMA map cannot
+// express (the caller falls back to the generic kernels).
+struct NgfBufs {
+  float *V, *G, *Nf, *Rho, *Z;
+  long long vlo, vhi, vstride, zlo, zhi, zstride;
+};
+
+template <int D, int KP>
+cudaError_t run_ngf_pass1_kp(const Launch& L, const Args& a, const NgfBufs& B, double* part, size_t part_cap,
+                             int* nblk) {
+  using C = TGX<KP>;
+  const long long npix = a.pix_hi - a.pix_lo;
+  if (npix <= 0 || a.K > KP) return cudaErrorNotSupported;
+  if (((a.pix_lo - B.zlo) * 4) % 16 || (B.zstride * 4) % 16 || (reinterpret_cast<uintptr_t>(B.Nf) & 15))
+    return cudaErrorNotSupported;
+  EncodeTiledFn fn = encode_tiled_fn();
+  if (!fn) return cudaErrorNotSupported;
+  CUtensorMap xmap;
+  memset(&xmap, 0, sizeof xmap);
+  cuuint64_t gdim[3] = {(cuuint64_t)npix, (cuuint64_t)D, (cuuint64_t)a.K};
+  cuuint64_t gstr[2] = {(cuuint64_t)B.zstride * 4, (cuuint64_t)D * B.zstride * 4};
+  cuuint32_t box[3] = {(cuuint32_t)C::TP, 1, (cuuint32_t)KP};
+  cuuint32_t es[3] = {1, 1, 1};
+  if (fn(&xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, B.Nf + (a.pix_lo - B.zlo), gdim, gstr, box, es,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorNotSupported;
+  // u and grad T over [vlo, vhi) (no shift: n only sees differences of u)
+  Args av = a;
+  av.pix_lo = B.vlo;
+  av.pix_hi = B.vhi;
+  av.shifts = nullptr;
+  constexpr int SPT = 4;
+  const dim3 sgrid((unsigned)((B.vhi - B.vlo + 256 * SPT - 1) / (256 * SPT)), (unsigned)a.K);
+  if (a.g.pow2) k_sample_v<D, true, SPT, true><<<sgrid, 256, 0, L.stream>>>(av, B.V, B.G, B.vstride);
+  else k_sample_v<D, false, SPT, true><<<sgrid, 256, 0, L.stream>>>(av, B.V, B.G, B.vstride);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const dim3 fgrid((unsigned)((B.zhi - B.zlo + 255) / 256), (unsigned)a.K);
+  k_ngf_feat<D><<<fgrid, 256, 0, L.stream>>>(a, B.V, B.vlo, B.vstride, B.Nf, B.Rho, B.zlo, B.zhi, B.zstride);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const size_t smem = tgx_smem<KP>();
+  e = cudaFuncSetAttribute(k_gram_tcx<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int ntx = (int)((npix + C::TP - 1) / C::TP);
+  const long long ntiles = (long long)ntx * D;
+  int grid = L.grid_override > 0 ? L.grid_override : L.sms;
+  if (grid > ntiles) grid = (int)ntiles;
+  const size_t stride = (size_t)KP * KP + 3 * KP;
+  if ((size_t)grid * stride > part_cap) grid = (int)(part_cap / stride);
+  Args b = a;
+  b.part = part;
+  k_gram_tcx<KP><<<grid, C::NT, smem, L.stream>>>(b, xmap, ntx, D);
+  *nblk = grid;
+  return cudaGetLastError();
+}
+
+template <int D>
+cudaError_t run_ngf_pass1(const Launch& L, const Args& a, const NgfBufs& B, double* part, size_t part_cap, int* nblk) {
+  return a.K <= 64 ? run_ngf_pass1_kp<D, 64>(L, a, B, part, part_cap, nblk)
+                   : run_ngf_pass1_kp<D, 128>(L, a, B, part, part_cap, nblk);
+}
+
+template <int D>
+cudaError_t run_ngf_pass2(const Launch& L, const Args& a, const NgfBufs& B) {
+  const int K = a.K;
+  const int groups = (K + NGF_JG - 1) / NGF_JG;
+  const int KP16 = groups * NGF_JG;
+  const size_t smem = ((size_t)K * KP16 + (size_t)K * D * NGF_ZP) * 4;
+  cudaError_t e = cudaFuncSetAttribute(k_ngf_z<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_ngf_z<D><<<(unsigned)((B.zhi - B.zlo + NGF_ZP - 1) / NGF_ZP), NGF_ZP * groups, smem, L.stream>>>(
+      a, B.Nf, B.Rho, B.zlo, B.zhi, B.zstride, B.Z);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const dim3 g2((unsigned)((a.pix_hi - a.pix_lo + 255) / 256), (unsigned)K);
+  k_ngf_adj_stream<D><<<g2, 256, 0, L.stream>>>(a, B.Z, B.zlo, B.zstride, B.G, B.vlo, B.vstride);
+  return cudaGetLastError();
+}
+cudaError_t ngf_pass1_d2(const Launch& L, const Args& a, const NgfBufs& B, double* part, size_t cap, int* nblk);
+cudaError_t ngf_pass1_d3(const Launch& L, const Args& a, const NgfBufs& B, double* part, size_t cap, int* nblk);
+cudaError_t ngf_pass2_d2(const Launch& L, const Args& a, const NgfBufs& B);
+cudaError_t ngf_pass2_d3(const Launch& L, const Args& a, const NgfBufs& B);
+
 cudaError_t pass1_split_d2(const Launch& L, const Args& a, float* V, float* G, long long vstride, double* part,
                            size_t cap, int* nblk);
 cudaError_t pass1_split_d3(const Launch& L, const Args& a, float* V, float* G, long long vstride, double* part,
