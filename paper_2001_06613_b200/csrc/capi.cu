@@ -45,6 +45,8 @@ struct sr_ctx {
   int tex_enabled = 0;  // SEQREG_B200_TEX=1: texture-gather sampling (measured slower on B200)
   int tc = 1;      // SEQREG_B200_TC=0: SIMT Gram instead of tcgen05 in pass 1
   int tc2 = 0;     // SEQREG_B200_TC2=1: tcgen05 pass 2
+  int mma = 1;     // SEQREG_B200_MMA: 1 = k_sample_v + k_gram_mma + k_pass2_mma, 2 = fused k_sample_gram,
+                   // 0 = k_sample_v + k_gram_tc (tcgen05) + k_pass2_stream
   int split = 1;   // SEQREG_B200_SPLIT=0: fused tensor-core pass 1 instead of sampling kernel + Gram kernel
   float* vbuf = nullptr;  // split pass 1: V = v - shift, [K][vstride]
   size_t vbuf_bytes = 0;
@@ -390,7 +392,13 @@ static int corr_partial_impl(sr_ctx* c, const sr_problem* p, double* raw, double
       G = c->gbuf;
     }
     c->vtag.valid = 0;
-    if (p->grid.ndim == 2) CK(pass1_split_d2(L, a, c->vbuf, G, vstride, c->part, c->part_cap, &nblk));
+    if (G && c->mma == 2)  // fused sampling + mma.sync Gram (engine_mma.cuh; measured slower)
+      CK(p->grid.ndim == 2 ? sample_gram_d2(L, a, c->vbuf, G, vstride, c->part, c->part_cap, &nblk)
+                           : sample_gram_d3(L, a, c->vbuf, G, vstride, c->part, c->part_cap, &nblk));
+    else if (G && c->mma)  // k_sample_v + mma.sync Gram kernel (engine_mma.cuh)
+      CK(p->grid.ndim == 2 ? sample_then_gram_d2(L, a, c->vbuf, G, vstride, c->part, c->part_cap, &nblk)
+                           : sample_then_gram_d3(L, a, c->vbuf, G, vstride, c->part, c->part_cap, &nblk));
+    else if (p->grid.ndim == 2) CK(pass1_split_d2(L, a, c->vbuf, G, vstride, c->part, c->part_cap, &nblk));
     else CK(pass1_split_d3(L, a, c->vbuf, G, vstride, c->part, c->part_cap, &nblk));
     set_vtag(c, p, vstride, G != nullptr);
   } else {
@@ -488,6 +496,8 @@ int sr_create(int32_t device, sr_ctx** out) {
     c->p2s = (ps && ps[0] == '0') ? 0 : 1;
     const char* t2 = getenv("SEQREG_B200_TC2");
     c->tc2 = (t2 && t2[0] == '1') ? 1 : 0;
+    const char* mm = getenv("SEQREG_B200_MMA");
+    c->mma = mm ? atoi(mm) : 1;
   }
   CK(cudaMalloc(&c->job_dev, sizeof(Job)));
   CK(cudaMalloc(&c->ticket, sizeof(unsigned)));
@@ -665,8 +675,13 @@ static int grad_impl(sr_ctx* c, const sr_problem* p, const double* stats, void* 
     a.o_off = g_off;
     a.o_stride = g_stride;
     if (reuse && p->dtype == SR_F32 && p->param == SR_DISPLACEMENT && p->k <= 32 && vtag_matches(c, p)) {
-      CK(d == 2 ? pass2_stream_d2(L, a, c->vbuf, c->gbuf, c->vtag.vstride)
-                : pass2_stream_d3(L, a, c->vbuf, c->gbuf, c->vtag.vstride));
+      const long long lim = 1LL << 31;  // k_pass2_mma uses 32-bit element offsets
+      if (c->mma && (long long)p->k * d * c->vtag.vstride < lim && (long long)p->k * d * g_stride < lim)
+        CK(d == 2 ? pass2_mma_d2(L, a, c->vbuf, c->gbuf, c->vtag.vstride)
+                  : pass2_mma_d3(L, a, c->vbuf, c->gbuf, c->vtag.vstride));
+      else
+        CK(d == 2 ? pass2_stream_d2(L, a, c->vbuf, c->gbuf, c->vtag.vstride)
+                  : pass2_stream_d3(L, a, c->vbuf, c->gbuf, c->vtag.vstride));
       return SR_OK;
     }
     CK(SR_SWITCH(p->dtype, d, pass2, p->feature, p->param, KP, L, a, c->aux, c->aux_cap, &nblk));

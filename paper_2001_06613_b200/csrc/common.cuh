@@ -79,6 +79,13 @@ __device__ __forceinline__ float ldg_hint(const float* p, uint64_t pol) {
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;\n" : "=f"(v) : "l"(p), "l"(pol));
   return v;
 }
+// the same load as a non-volatile asm: the compiler may schedule it across other memory operations
+// (use only for data no kernel in flight writes)
+__device__ __forceinline__ float ldg_hint_nv(const float* p, uint64_t pol) {
+  float v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;\n" : "=f"(v) : "l"(p), "l"(pol));
+  return v;
+}
 __device__ __forceinline__ float4 ldg4_hint(const float* p, uint64_t pol) {
   float4 v;
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;\n"

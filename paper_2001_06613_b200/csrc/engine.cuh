@@ -551,12 +551,21 @@ __device__ void finalize_block(const double* __restrict__ raw, const Job* job, i
   __shared__ double red[1024];
   const int tid = threadIdx.x, nt = blockDim.x;
   const StatsLayout L(K);
-  const double* G = raw;
   const double N = n_total;
+  // one round trip for every input: the raw Gram into shared memory (C is formed in place), the
+  // per-frame sums / extrema, weights, frame indices and shifts into registers of threads < K
+  for (int e = tid; e < K * K; e += nt) Cmat[e] = __ldcg(raw + e);
+  double si = 0.0, vmx = 0.0, vmnn = 0.0, wt = 0.0, sh = 0.0;
   if (tid < K) {
-    const double gii = __ldcg(G + tid * K + tid);
-    const double si = __ldcg(raw + K * K + tid);
-    const double vmx = __ldcg(raw + K * K + K + tid), vmnn = __ldcg(raw + K * K + 2 * K + tid);
+    si = __ldcg(raw + K * K + tid);
+    vmx = __ldcg(raw + K * K + K + tid);
+    vmnn = __ldcg(raw + K * K + 2 * K + tid);
+    wt = job->weights[tid];
+    sh = (feat == NCC && shifts) ? (double)shifts[job->frame_index[tid]] : 0.0;
+  }
+  __syncthreads();
+  if (tid < K) {
+    const double gii = Cmat[tid * K + tid];
     const double amax = fmax(vmx, vmnn);  // max |v|
     double sg, m = 0.0, thr;
     int dg;
@@ -580,23 +589,23 @@ __device__ void finalize_block(const double* __restrict__ raw, const Job* job, i
     mu[tid] = m;
     sv[tid] = si;
     deg[tid] = dg;
-    w[tid] = job->weights[tid];
-    const double sh = (feat == NCC && shifts) ? (double)shifts[job->frame_index[tid]] : 0.0;
+    w[tid] = wt;
     stats[L.sigma + tid] = sg;
     stats[L.mean + tid] = feat == NCC ? sh + m : 0.0;
     stats[L.vmax + tid] = amax;
     stats[L.degen + tid] = dg;
-    stats[L.weights + tid] = w[tid];
+    stats[L.weights + tid] = wt;
     stats[L.shift + tid] = sh;
   }
   __syncthreads();
   // C (upper triangle computed once, mirrored -> exactly symmetric, similarity.py:155)
+  // (in place: the thread of (i, j), i <= j, reads G_ij and writes C_ij and C_ji; G_ji (i < j) is never read)
   for (int e = tid; e < K * K; e += nt) {
     const int i = e / K, j = e % K;
     if (i > j) continue;
     double c = 0.0;
     if (!deg[i] && !deg[j]) {
-      const double gij = __ldcg(G + i * K + j);
+      const double gij = Cmat[i * K + j];
       const double num = feat == NCC ? gij - sv[i] * mu[j] : gij;
       c = num * (isg[i] * isg[j]);
     }
@@ -669,6 +678,110 @@ __device__ void finalize_block(const double* __restrict__ raw, const Job* job, i
   }
 }
 
+// Finalize for K <= 32 with 1024 threads: warp i owns row i, lane j column j, so that every per-frame
+// quantity a thread needs is either its own lane's (frame j) or a shuffle from lane i (frame i):
+// one global round trip, two CTA barriers.  C_ij is formed from the upper element G[min][max] with
+// the factors in (min, max) order, so C is exactly symmetric; c_j and dcol_j are row sums of warp j
+// (C symmetric), in the generic finalize's lane order and xor tree (bitwise the same numbers).
+template <typename T>
+__device__ void finalize_k32(const double* __restrict__ raw, const Job* job, int K, int feat, int D,
+                             double n_total, double h, const T* shifts, double* __restrict__ stats) {
+  __shared__ double colp[32][33];  // M'_ij mu_i, for the column sums of beta'
+  __shared__ double dcol[32];
+  const int tid = threadIdx.x, lane = tid & 31, i = tid >> 5;
+  const StatsLayout L(K);
+  const double N = n_total;
+  const int j = lane;
+  const bool act = i < K && j < K;
+  const int lo = min(i, j), hi = max(i, j);
+  // ---- inputs (one round trip): the Gram element, frame j's sums / extrema / weight / shift
+  double gij = 0.0, gjj = 0.0, sj = 0.0, vmx = 0.0, vmnn = 0.0, wj = 0.0, shj = 0.0;
+  if (act) gij = __ldcg(raw + lo * K + hi);
+  if (j < K) {
+    gjj = __ldcg(raw + j * K + j);
+    sj = __ldcg(raw + K * K + j);
+    vmx = __ldcg(raw + K * K + K + j);
+    vmnn = __ldcg(raw + K * K + 2 * K + j);
+    wj = job->weights[j];
+    shj = (feat == NCC && shifts) ? (double)shifts[job->frame_index[j]] : 0.0;
+  }
+  // ---- per-frame statistics of frame j (every warp, redundantly)
+  const double amax = fmax(vmx, vmnn);
+  double sg = 0.0, mj = 0.0;
+  int dg = 1;
+  if (j < K) {
+    if (feat == NCC) {
+      mj = sj / N;
+      const double var = gjj - sj * mj;
+      sg = sqrt(fmax(var, 0.0));
+      const double thr = 1e-12 * sqrt(N) * (1.0 + amax);  // similarity.py:84-86
+      const bool constant = vmx == -vmnn;  // exactly constant frame (see finalize_block)
+      dg = !(sg >= thr) || constant;
+      if (constant) sg = 0.0;
+    } else {
+      sg = sqrt(fmax(gjj, 0.0));
+      const double thr = 1e-12 * sqrt(N * D) * (1.0 + amax);
+      dg = !(sg >= thr);
+    }
+  }
+  const double isgj = dg ? 0.0 : 1.0 / sg;
+  // frame i's (= row) quantities from lane i
+  const double isgi = __shfl_sync(0xffffffffu, isgj, i & 31);
+  const double si = __shfl_sync(0xffffffffu, sj, i & 31), mi = __shfl_sync(0xffffffffu, mj, i & 31);
+  const double wi = __shfl_sync(0xffffffffu, wj, i & 31);
+  const int dgi = __shfl_sync(0xffffffffu, dg, i & 31);
+  if (i == 0 && j < K) {
+    stats[L.sigma + j] = sg;
+    stats[L.mean + j] = feat == NCC ? shj + mj : 0.0;
+    stats[L.vmax + j] = amax;
+    stats[L.degen + j] = dg;
+    stats[L.weights + j] = wj;
+    stats[L.shift + j] = shj;
+  }
+  // ---- C_ij (exactly symmetric: the (lo, hi) formula)
+  double c = 0.0;
+  if (act && !dg && !dgi) {
+    const double s_lo = lo == i ? si : sj, m_hi = hi == j ? mj : mi;
+    const double i_lo = lo == i ? isgi : isgj, i_hi = hi == j ? isgj : isgi;
+    const double num = feat == NCC ? gij - s_lo * m_hi : gij;
+    c = num * (i_lo * i_hi);
+  }
+  if (act) stats[L.C + i * K + j] = c;
+  // ---- c_i = sum_j w_j C_ij^2 and dcol_i = sum_{j != i} w_j w_i C_ij^2 (row sums of warp i)
+  const double wc2 = act ? wj * c * c : 0.0;
+  const double cp = warp_sum(wc2);
+  const double dp = warp_sum(act && j != i ? wc2 * wi : 0.0);
+  if (lane == 0 && i < 32) dcol[i] = i < K ? dp : 0.0;
+  // ---- M'_ij = -4 h w_j (w_i C_ij / sig_i - delta_ij c_j / sig_j) / sig_j
+  double m = 0.0;
+  if (act && !dg && !dgi) {
+    double t = wi * c * isgi;
+    if (i == j) t -= cp * isgj;
+    m = -4.0 * h * wj * t * isgj;
+  }
+  if (act) {
+    stats[L.M + i * K + j] = m;
+    reinterpret_cast<float*>(stats + L.Mf)[i * K + j] = (float)m;
+  }
+  colp[i & 31][j] = m * mi;
+  __syncthreads();
+  // ---- beta'_j = -sum_i M'_ij mu_i (warp j sums column j over lanes i); D
+  if (i < K) {
+    const double bp = warp_sum(lane < K ? colp[lane][i] : 0.0);
+    if (lane == 0) stats[L.beta + i] = feat == NCC ? -bp : 0.0;
+  }
+  if (i == 0) {
+    const double dsum = warp_sum(dcol[lane]);
+    const double sw = warp_sum(j < K ? wj : 0.0), sw2 = warp_sum(j < K ? wj * wj : 0.0);
+    if (lane == 0) {
+      stats[0] = fmax(0.0, h * ((sw * sw - sw2) - dsum));
+      stats[1] = K;
+      stats[2] = N;
+      stats[3] = h;
+    }
+  }
+}
+
 // Cross-CTA reduction of the pass-1 partials (fixed order: warp w of a block sums CTAs
 // w, w+32, ..., then warp 0 combines the 32 warp sums in order) packed straight into the
 // caller's raw layout; the last block to finish (atomic ticket) writes the count and, when
@@ -721,7 +834,8 @@ __global__ void __launch_bounds__(1024) k_reduce_finalize(const double* __restri
     *ticket = 0u;
   }
   if (!do_final) return;
-  finalize_block<T>(raw, job, K, feat, D, (double)count, h, shifts, stats, reinterpret_cast<double*>(dsm));
+  if (K <= 32 && blockDim.x == 1024) finalize_k32<T>(raw, job, K, feat, D, (double)count, h, shifts, stats);
+  else finalize_block<T>(raw, job, K, feat, D, (double)count, h, shifts, stats, reinterpret_cast<double*>(dsm));
 }
 
 // Finalize only (sharded path: raw sums all-reduced by the caller).
@@ -730,7 +844,8 @@ __global__ void __launch_bounds__(1024) k_finalize(const double* __restrict__ ra
                                                    int feat, int D, double n_total, double h,
                                                    const T* shifts, double* __restrict__ stats) {
   extern __shared__ __align__(16) unsigned char dsm[];
-  finalize_block<T>(raw, job, K, feat, D, n_total, h, shifts, stats, reinterpret_cast<double*>(dsm));
+  if (K <= 32 && blockDim.x == 1024) finalize_k32<T>(raw, job, K, feat, D, n_total, h, shifts, stats);
+  else finalize_block<T>(raw, job, K, feat, D, n_total, h, shifts, stats, reinterpret_cast<double*>(dsm));
 }
 
 // ===================================================================== pass 2

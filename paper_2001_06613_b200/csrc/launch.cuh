@@ -382,6 +382,17 @@ cudaError_t run_pass2_stream(const Launch& L, const Args& a, const float* V, con
   return cudaGetLastError();
 }
 cudaError_t pass2_stream_d2(const Launch& L, const Args& a, const float* V, const float* G, long long vstride);
+// engine_mma.cuh (mma_pass.cu): fused sampling + mma.sync Gram pass 1, mma.sync streaming pass 2
+cudaError_t sample_gram_d2(const Launch& L, const Args& a, float* V, float* G, long long vstride, double* part,
+                           size_t cap, int* nblk);
+cudaError_t sample_gram_d3(const Launch& L, const Args& a, float* V, float* G, long long vstride, double* part,
+                           size_t cap, int* nblk);
+cudaError_t sample_then_gram_d2(const Launch& L, const Args& a, float* V, float* G, long long vstride, double* part,
+                                size_t cap, int* nblk);
+cudaError_t sample_then_gram_d3(const Launch& L, const Args& a, float* V, float* G, long long vstride, double* part,
+                                size_t cap, int* nblk);
+cudaError_t pass2_mma_d2(const Launch& L, const Args& a, const float* V, const float* G, long long vstride);
+cudaError_t pass2_mma_d3(const Launch& L, const Args& a, const float* V, const float* G, long long vstride);
 cudaError_t pass2_stream_d3(const Launch& L, const Args& a, const float* V, const float* G, long long vstride);
 
 // Dispatch over (FEAT, PARAM, KP) for fixed (T, D).

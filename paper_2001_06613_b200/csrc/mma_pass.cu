@@ -1,0 +1,101 @@
+// Launchers for engine_mma.cuh (fp32 NCC displacement fields, K <= 32, 2-D and 3-D).
+#include <cstdio>
+#include <cstdlib>
+#include "engine_mma.cuh"
+#include "launch.cuh"
+
+namespace sr {
+
+template <int D>
+static cudaError_t run_sample_gram(const Launch& L, const Args& a, float* V, float* G, long long vstride,
+                                   double* part, size_t part_cap, int* nblk) {
+  const long long npix = a.pix_hi - a.pix_lo;
+  if (npix <= 0 || a.K > SG::KP) return cudaErrorInvalidValue;
+  const long long ntiles = (npix + SG::TP - 1) / SG::TP;
+  // SEQREG_B200_SGB: minimum resident CTAs per SM the kernel is compiled for (register budget)
+  static const int minb = getenv("SEQREG_B200_SGB") ? atoi(getenv("SEQREG_B200_SGB")) : 4;
+  auto kern = a.g.pow2 ? (minb == 3 ? k_sample_gram<D, true, 3> : minb == 2 ? k_sample_gram<D, true, 2> : k_sample_gram<D, true, 4>)
+                       : (minb == 3 ? k_sample_gram<D, false, 3> : minb == 2 ? k_sample_gram<D, false, 2> : k_sample_gram<D, false, 4>);
+  int grid = occupancy_grid(L, kern, SG::NT, 0, ntiles);
+  const size_t stride = (size_t)SG::KP * SG::KP + 3 * SG::KP;
+  if ((size_t)grid * stride > part_cap) grid = (int)(part_cap / stride);
+  Args b = a;
+  b.part = part;
+  kern<<<grid, SG::NT, 0, L.stream>>>(b, V, G, vstride);
+  *nblk = grid;
+  return cudaGetLastError();
+}
+
+// split pass 1: k_sample_v (V = v - shift, grad T) then k_gram_mma (Gram + per-frame stats of V)
+template <int D>
+static cudaError_t run_sample_then_gram(const Launch& L, const Args& a, float* V, float* G, long long vstride,
+                                        double* part, size_t part_cap, int* nblk) {
+  const long long npix = a.pix_hi - a.pix_lo;
+  if (npix <= 0 || a.K > GMM::KP) return cudaErrorInvalidValue;
+  constexpr int SPT = 4;
+  const dim3 sgrid((unsigned)((npix + 256 * SPT - 1) / (256 * SPT)), (unsigned)a.K);
+  if (a.g.pow2) k_sample_v<D, true, SPT, true><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
+  else k_sample_v<D, false, SPT, true><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const size_t smem = 4 * (size_t)GMM::KP * GMM::LD * sizeof(float);
+  e = cudaFuncSetAttribute(k_gram_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const long long ntiles = (npix + GMM::TP - 1) / GMM::TP;
+  int grid = occupancy_grid(L, k_gram_mma, GMM::NT, smem, ntiles);
+  const size_t stride = (size_t)GMM::KP * GMM::KP + 3 * GMM::KP;
+  if ((size_t)grid * stride > part_cap) grid = (int)(part_cap / stride);
+  Args b = a;
+  b.part = part;
+  k_gram_mma<<<grid, GMM::NT, smem, L.stream>>>(b, V, vstride);
+  *nblk = grid;
+  return cudaGetLastError();
+}
+
+template <int D>
+static cudaError_t run_pass2_mma(const Launch& L, const Args& a, const float* V, const float* G, long long vstride) {
+  const long long npix = a.pix_hi - a.pix_lo;
+  if (npix <= 0) return cudaSuccess;
+  if (getenv("SEQREG_B200_P2BULK") && (vstride & 3) == 0 && (reinterpret_cast<uintptr_t>(V) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(G) & 15) == 0) {
+    using C = P2B<D>;
+    const size_t smem = C::smem();
+    cudaError_t e = cudaFuncSetAttribute(k_pass2_bulk<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const long long nblk = (npix + C::PW - 1) / C::PW;
+    const long long want = (nblk + C::WPC - 1) / C::WPC;
+    const int grid = occupancy_grid(L, k_pass2_bulk<D>, C::NT, smem, want);
+    k_pass2_bulk<D><<<grid, C::NT, smem, L.stream>>>(a, V, G, vstride);
+    return cudaGetLastError();
+  }
+  const long long nblk = (npix + P2M::PW - 1) / P2M::PW;
+  const long long want = (nblk + P2M::NT / 32 - 1) / (P2M::NT / 32);
+  const int grid = occupancy_grid(L, k_pass2_mma<D>, P2M::NT, 0, want);
+  k_pass2_mma<D><<<grid, P2M::NT, 0, L.stream>>>(a, V, G, vstride);
+  return cudaGetLastError();
+}
+
+cudaError_t sample_gram_d2(const Launch& L, const Args& a, float* V, float* G, long long vstride, double* part,
+                           size_t cap, int* nblk) {
+  return run_sample_gram<2>(L, a, V, G, vstride, part, cap, nblk);
+}
+cudaError_t sample_gram_d3(const Launch& L, const Args& a, float* V, float* G, long long vstride, double* part,
+                           size_t cap, int* nblk) {
+  return run_sample_gram<3>(L, a, V, G, vstride, part, cap, nblk);
+}
+cudaError_t sample_then_gram_d2(const Launch& L, const Args& a, float* V, float* G, long long vstride, double* part,
+                                size_t cap, int* nblk) {
+  return run_sample_then_gram<2>(L, a, V, G, vstride, part, cap, nblk);
+}
+cudaError_t sample_then_gram_d3(const Launch& L, const Args& a, float* V, float* G, long long vstride, double* part,
+                                size_t cap, int* nblk) {
+  return run_sample_then_gram<3>(L, a, V, G, vstride, part, cap, nblk);
+}
+cudaError_t pass2_mma_d2(const Launch& L, const Args& a, const float* V, const float* G, long long vstride) {
+  return run_pass2_mma<2>(L, a, V, G, vstride);
+}
+cudaError_t pass2_mma_d3(const Launch& L, const Args& a, const float* V, const float* G, long long vstride) {
+  return run_pass2_mma<3>(L, a, V, G, vstride);
+}
+
+}  // namespace sr
