@@ -228,31 +228,36 @@ constexpr int GMM_LD = GMM::LD;
 // rows 0..15 and 16..31 delivers {V[g][t], V[g+8][t], V[g][t+4], V[g+8][t+4]} of each 16-row block:
 // the A operand of block row m, and (a0, a2) / (a1, a3) = the B operand of n-tile 2 m / 2 m + 1.
 // (m16n8k4, whose operands the quad holds in place, measured slower — half the work per HMMA.)
-__device__ __forceinline__ void gram_eighth(float (&acc)[6][4], uint32_t addr) {
+__device__ __forceinline__ void gram_eighth(float (&acc)[6][4], uint32_t addr, uint32_t baddr) {
   constexpr uint32_t LDB = GMM_LD * 4, LOB = 2 * 32 * GMM_LD * 4;  // row bytes; hi -> lo offset
 #pragma unroll
   for (int kq = 0; kq < 2; ++kq) {
-    uint32_t FH[2][4], FL[2][4];
+    // A-order quads {V[g][t], V[g+8][t], V[g][t+4], V[g+8][t+4]} and B-order quads
+    // {V[g][t], V[g][t+4], V[g+8][t], V[g+8][t+4]} (B of n-tile 2m = regs 0, 1; 2m + 1 = regs 2, 3):
+    // two more ldmatrix per k-step instead of the register moves that would pair (a0, a2) / (a1, a3)
+    uint32_t FH[2][4], FL[2][4], BH[2][4], BL[2][4];
 #pragma unroll
     for (int m2 = 0; m2 < 2; ++m2) {
       ldsm_x4(FH[m2], addr + m2 * 16 * LDB + 32 * kq);
       ldsm_x4(FL[m2], addr + m2 * 16 * LDB + LOB + 32 * kq);
+      ldsm_x4(BH[m2], baddr + m2 * 16 * LDB + 32 * kq);
+      ldsm_x4(BL[m2], baddr + m2 * 16 * LDB + LOB + 32 * kq);
     }
     // block b: (m, n) = (0, 0..3), (1, 2), (1, 3)
 #pragma unroll
     for (int b = 0; b < 6; ++b) {
       const int m = b < 4 ? 0 : 1, n = b < 4 ? b : b - 2;
-      mma_tf32(acc[b], FH[m], FH[n >> 1][n & 1], FH[n >> 1][2 + (n & 1)]);
+      mma_tf32(acc[b], FH[m], BH[n >> 1][2 * (n & 1)], BH[n >> 1][2 * (n & 1) + 1]);
     }
 #pragma unroll
     for (int b = 0; b < 6; ++b) {
       const int m = b < 4 ? 0 : 1, n = b < 4 ? b : b - 2;
-      mma_tf32(acc[b], FL[m], FH[n >> 1][n & 1], FH[n >> 1][2 + (n & 1)]);
+      mma_tf32(acc[b], FL[m], BH[n >> 1][2 * (n & 1)], BH[n >> 1][2 * (n & 1) + 1]);
     }
 #pragma unroll
     for (int b = 0; b < 6; ++b) {
       const int m = b < 4 ? 0 : 1, n = b < 4 ? b : b - 2;
-      mma_tf32(acc[b], FH[m], FL[n >> 1][n & 1], FL[n >> 1][2 + (n & 1)]);
+      mma_tf32(acc[b], FH[m], BL[n >> 1][2 * (n & 1)], BL[n >> 1][2 * (n & 1) + 1]);
     }
   }
 }
@@ -282,7 +287,8 @@ __global__ void __launch_bounds__(GMM::NT, 2) k_gram_mma(const Args a, const flo
   // ldmatrix row addresses (bytes, buffer 0, rows 0.., k-step 0): lane L feeds row L & 7 of matrix L >> 3
   const int lr = lane & 7, lj = lane >> 3;
   const uint32_t sbase = smem_u32(gmm_smem);
-  const uint32_t aoff = (uint32_t)(((lr + 8 * (lj & 1)) * LD + 4 * (lj >> 1)) * 4);
+  const uint32_t aoff = (uint32_t)(((lr + 8 * (lj & 1)) * LD + 4 * (lj >> 1)) * 4);  // A-order
+  const uint32_t boff = (uint32_t)(((lr + 8 * (lj >> 1)) * LD + 4 * (lj & 1)) * 4);  // B-order
   // rows r0 .. r0+3, columns 4 lane .. 4 lane + 3 of tile `tile` (zero past K and past the slab)
   auto load = [&](long long tile, float4 (&x)[4]) {
     const long long c0 = tile * TP + 4 * lane;
@@ -338,7 +344,7 @@ __global__ void __launch_bounds__(GMM::NT, 2) k_gram_mma(const Args a, const flo
     // ---- prefetch the next tile's rows, then the MMAs of this tile (gram_eighth)
     if (tile + gridDim.x < ntiles) load(tile + gridDim.x, x);
     const uint32_t bb = sbase + (uint32_t)(buf * KP * LD * 4);
-    gram_eighth(acc, bb + aoff + (uint32_t)(64 * warp));
+    gram_eighth(acc, bb + aoff + (uint32_t)(64 * warp), bb + boff + (uint32_t)(64 * warp));
     ++nt;
     if ((nt & 7) == 0 || tile + gridDim.x >= ntiles) {  // fp32 over <= 8 tiles (128 pixels), fp64 across
 #pragma unroll
@@ -395,6 +401,221 @@ __device__ __forceinline__ void stsm_x4(uint32_t addr, float c0, float c1, float
   asm volatile("stmatrix.sync.aligned.m8n8.x4.shared.b16 [%0], {%1,%2,%3,%4};\n" ::"r"(addr), "r"(__float_as_uint(c0)),
                "r"(__float_as_uint(c1)), "r"(__float_as_uint(c2)), "r"(__float_as_uint(c3))
                : "memory");
+}
+
+// Split pass 1, Gram kernel, TMA-fed (default): persistent CTAs over 128-pixel tiles; one thread
+// streams [32 frames x 32 pixels] boxes of V (SWIZZLE_128B, zero fill past K and past the slab) into an
+// NST-stage ring (full: TMA transaction barrier, empty: one arrival per warp), so NST tiles are in
+// flight per CTA and no thread holds in-flight data.  Warp w owns pixels 16 w .. 16 w + 15 of every
+// tile (2 k-steps): ldmatrix.x4 of the raw fp32 rows in A order {V[g][t], V[g+8][t], V[g][t+4],
+// V[g+8][t+4]} and in B order {V[g][t], V[g][t+4], V[g+8][t], V[g+8][t+4]}, hi/lo split in registers,
+// the six upper m16n8 blocks with 3 HMMAs each (fp32 per <= 8 tiles, fp64 across), per-frame sum /
+// max / min from the A-order fragments (every element lies in exactly one of them).
+struct GTM {
+  static constexpr int KP = 32, TP = 128, NT = 256, NST = 4, BOXP = 32;
+  static constexpr int SBYTES = KP * TP * 4;  // one stage: 4 boxes of [32 rows x 128 B]
+};
+constexpr size_t gtm_smem() { return 1024 + (size_t)GTM::NST * GTM::SBYTES + 256; }
+
+// hi = v with the 13 low mantissa bits cleared (exact in tf32; one LOP3 instead of the ~4-instruction
+// cvt.rna), lo = v - hi exactly (|lo| < 2^-10 |v|, truncated to tf32 by the MMA: 2^-20 relative).
+__device__ __forceinline__ void split_q(const uint32_t (&q)[4], uint32_t (&h)[4], uint32_t (&l)[4]) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    h[u] = q[u] & 0xffffe000u;
+    l[u] = __float_as_uint(__uint_as_float(q[u]) - __uint_as_float(h[u]));
+  }
+}
+
+__global__ void __launch_bounds__(GTM::NT, 2) k_gram_tma(const Args a, const __grid_constant__ CUtensorMap vmap) {
+  constexpr int KP = GTM::KP, TP = GTM::TP, NST = GTM::NST;
+  extern __shared__ __align__(1024) unsigned char gtm_sh[];
+  unsigned char* base = gtm_sh + ((1024 - (smem_u32(gtm_sh) & 1023)) & 1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)NST * GTM::SBYTES);
+  uint64_t* empty = full + NST;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int K = a.K;
+  const long long npix = a.pix_hi - a.pix_lo;
+  const long long ntiles = (npix + TP - 1) / TP;
+  const long long nloc = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  if (tid == 0) {
+    for (int s2 = 0; s2 < NST; ++s2) {
+      mbar_init(&full[s2], 1);
+      mbar_init(&empty[s2], GTM::NT / 32);
+    }
+    fence_mbar_init();
+    tma_prefetch_desc(&vmap);
+  }
+  __syncthreads();
+  auto issue = [&](long long n, int s2) {
+    const int x0 = (int)((blockIdx.x + n * gridDim.x) * TP);
+    unsigned char* st = base + (size_t)s2 * GTM::SBYTES;
+    mbar_arrive_expect_tx(&full[s2], (uint32_t)GTM::SBYTES);
+#pragma unroll
+    for (int b = 0; b < TP / GTM::BOXP; ++b) tma_load_2d(st + b * 4096, &vmap, x0 + GTM::BOXP * b, 0, &full[s2]);
+  };
+  if (tid == 0)
+    for (long long n = 0; n < nloc && n < NST; ++n) issue(n, (int)n);
+  // this warp's ldmatrix row addresses inside a stage: box warp >> 1, pixel columns 16 (warp & 1) + 8 kq
+  const int lr = lane & 7, lj = lane >> 3;
+  uint32_t aadr[2][2], badr[2][2];  // [m][kq], swizzled (16-byte chunk ^ (row & 7))
+#pragma unroll
+  for (int m = 0; m < 2; ++m)
+#pragma unroll
+    for (int kq = 0; kq < 2; ++kq) {
+      const int c = 16 * (warp & 1) + 8 * kq;
+      const int ra = 16 * m + lr + 8 * (lj & 1), ca = c + 4 * (lj >> 1);
+      const int rb = 16 * m + lr + 8 * (lj >> 1), cb = c + 4 * (lj & 1);
+      aadr[m][kq] = (uint32_t)((warp >> 1) * 4096 + ra * 128 + (((ca >> 2) ^ (ra & 7)) << 4));
+      badr[m][kq] = (uint32_t)((warp >> 1) * 4096 + rb * 128 + (((cb >> 2) ^ (rb & 7)) << 4));
+    }
+  const uint32_t sb = smem_u32(base);
+  float acc[6][4] = {};
+  double gacc[6][4] = {};
+  float fs[2][2] = {}, fmx[2][2], fmn[2][2];  // [m][h]: rows 16 m + g + 8 h
+  double ds[2][2] = {};
+#pragma unroll
+  for (int m = 0; m < 2; ++m)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      fmx[m][h] = -INFINITY;
+      fmn[m][h] = INFINITY;
+    }
+  for (long long n = 0; n < nloc; ++n) {
+    const int s2 = (int)(n % NST);
+    const uint32_t st = sb + (uint32_t)(s2 * GTM::SBYTES);
+    const long long p0 = (blockIdx.x + n * gridDim.x) * TP + 16 * warp;  // this warp's first pixel
+    mbar_wait(&full[s2], (uint32_t)((n / NST) & 1));
+    uint32_t QA[2][2][4], QB[2][2][4];
+#pragma unroll
+    for (int kq = 0; kq < 2; ++kq)
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        ldsm_x4(QA[kq][m], st + aadr[m][kq]);
+        ldsm_x4(QB[kq][m], st + badr[m][kq]);
+      }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s2]);
+    if (tid == 0 && n + NST < nloc) {  // refill this stage once every warp has read it
+      mbar_wait(&empty[s2], (uint32_t)((n / NST) & 1));
+      issue(n + NST, s2);
+    }
+#pragma unroll
+    for (int kq = 0; kq < 2; ++kq) {
+      // per-frame statistics from the A-order fragments: rows 16 m + g (+ 8), pixels p0 + 8 kq + t (+ 4)
+      const long long pc = p0 + 8 * kq + t;
+      const bool ok0 = pc < npix, ok1 = pc + 4 < npix;
+#pragma unroll
+      for (int m = 0; m < 2; ++m)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const float v0 = __uint_as_float(QA[kq][m][h]), v1 = __uint_as_float(QA[kq][m][2 + h]);
+          fs[m][h] += v0 + v1;  // zero past the slab
+          if (ok0) {
+            fmx[m][h] = fmaxf(fmx[m][h], v0);
+            fmn[m][h] = fminf(fmn[m][h], v0);
+          }
+          if (ok1) {
+            fmx[m][h] = fmaxf(fmx[m][h], v1);
+            fmn[m][h] = fminf(fmn[m][h], v1);
+          }
+        }
+      uint32_t AH[2][4], AL[2][4], BH[2][4], BL[2][4];
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        split_q(QA[kq][m], AH[m], AL[m]);
+        split_q(QB[kq][m], BH[m], BL[m]);
+      }
+      // block b: (m, n) = (0, 0..3), (1, 2), (1, 3); B of n-tile nn = BX[nn >> 1][2 (nn & 1) + 0, 1]
+#pragma unroll
+      for (int b = 0; b < 6; ++b) {
+        const int m = b < 4 ? 0 : 1, nn = b < 4 ? b : b - 2;
+        mma_tf32(acc[b], AH[m], BH[nn >> 1][2 * (nn & 1)], BH[nn >> 1][2 * (nn & 1) + 1]);
+      }
+#pragma unroll
+      for (int b = 0; b < 6; ++b) {
+        const int m = b < 4 ? 0 : 1, nn = b < 4 ? b : b - 2;
+        mma_tf32(acc[b], AL[m], BH[nn >> 1][2 * (nn & 1)], BH[nn >> 1][2 * (nn & 1) + 1]);
+      }
+#pragma unroll
+      for (int b = 0; b < 6; ++b) {
+        const int m = b < 4 ? 0 : 1, nn = b < 4 ? b : b - 2;
+        mma_tf32(acc[b], AH[m], BL[nn >> 1][2 * (nn & 1)], BL[nn >> 1][2 * (nn & 1) + 1]);
+      }
+    }
+    if ((n & 7) == 7 || n == nloc - 1) {  // fp32 over <= 8 tiles (128 pixels per warp), fp64 across
+#pragma unroll
+      for (int b = 0; b < 6; ++b)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          gacc[b][r] += (double)acc[b][r];
+          acc[b][r] = 0.f;
+        }
+#pragma unroll
+      for (int m = 0; m < 2; ++m)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          ds[m][h] += (double)fs[m][h];
+          fs[m][h] = 0.f;
+        }
+    }
+  }
+  // ---- CTA reduction (fixed order) through shared memory (the stages are no longer in use)
+  __syncthreads();
+  double* red = reinterpret_cast<double*>(base);  // [warp 8][block 6][r 4][lane 32], then stats
+#pragma unroll
+  for (int b = 0; b < 6; ++b)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) red[((warp * 6 + b) * 4 + r) * 32 + lane] = gacc[b][r];
+  // per-frame stats: reduce over the 4 lanes t of a row (xor tree), then over warps in smem
+  double* rs = red + 8 * 6 * 4 * 32;  // [warp 8][row 32] x {sum, max, -min}
+#pragma unroll
+  for (int m = 0; m < 2; ++m)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double sv = ds[m][h];
+      float mx = fmx[m][h], mn = fmn[m][h];
+#pragma unroll
+      for (int o = 1; o <= 2; o <<= 1) {
+        sv += __shfl_xor_sync(0xffffffffu, sv, o);
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      }
+      if (t == 0) {
+        const int row = 16 * m + g + 8 * h;
+        rs[(warp * 32 + row) * 3 + 0] = sv;
+        rs[(warp * 32 + row) * 3 + 1] = (double)mx;
+        rs[(warp * 32 + row) * 3 + 2] = (double)mn;
+      }
+    }
+  __syncthreads();
+  double* out = a.part + (size_t)blockIdx.x * (KP * KP + 3 * KP);
+  for (int e = tid; e < 6 * 4 * 32; e += GTM::NT) {
+    double v = red[e];
+#pragma unroll
+    for (int w2 = 1; w2 < 8; ++w2) v += red[w2 * 6 * 4 * 32 + e];
+    const int b = e >> 7, r = (e >> 5) & 3, ln = e & 31;
+    const int m = b < 4 ? 0 : 1, nn = b < 4 ? b : b - 2;
+    const int i = 16 * m + (ln >> 2) + 8 * (r >> 1), j = 8 * nn + 2 * (ln & 3) + (r & 1);
+    out[i * KP + j] = v;
+    if (j >= 16 && i < 16) out[j * KP + i] = v;  // mirror of the strictly-upper blocks (0, 2), (0, 3)
+  }
+  if (tid < KP) {
+    const int k = tid;
+    double sv = 0.0, mx = -INFINITY, mn = INFINITY;
+#pragma unroll
+    for (int w2 = 0; w2 < 8; ++w2) {
+      sv += rs[(w2 * 32 + k) * 3 + 0];
+      mx = fmax(mx, rs[(w2 * 32 + k) * 3 + 1]);
+      mn = fmin(mn, rs[(w2 * 32 + k) * 3 + 2]);
+    }
+    const float* shifts = reinterpret_cast<const float*>(a.shifts);
+    const double sh = (k < K && shifts) ? (double)shifts[a.job->frame_index[k]] : 0.0;
+    out[KP * KP + k] = k < K ? sv : 0.0;
+    out[KP * KP + KP + k] = mx + sh;
+    out[KP * KP + 2 * KP + k] = -(mn + sh);
+  }
 }
 
 // Pass 2 (streaming, after a split pass 1 on the same y; default).  Warp = 8 consecutive pixels per
@@ -490,9 +711,10 @@ __global__ void __launch_bounds__(P2M::NT, 3) k_pass2_mma(const Args a, const fl
     }
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks) {
-      const float h0 = to_tf32(bv[ks][0]), h1 = to_tf32(bv[ks][1]);
-      const uint32_t bh0 = __float_as_uint(h0), bh1 = __float_as_uint(h1);
-      const uint32_t bl0 = __float_as_uint(bv[ks][0] - h0), bl1 = __float_as_uint(bv[ks][1] - h1);
+      // hi by truncation (exact in tf32, one LOP3), lo = v - hi exactly (see split_q)
+      const uint32_t bh0 = __float_as_uint(bv[ks][0]) & 0xffffe000u, bh1 = __float_as_uint(bv[ks][1]) & 0xffffe000u;
+      const uint32_t bl0 = __float_as_uint(bv[ks][0] - __uint_as_float(bh0));
+      const uint32_t bl1 = __float_as_uint(bv[ks][1] - __uint_as_float(bh1));
 #pragma unroll
       for (int m = 0; m < 2; ++m) {
         const float4 ah = Ah[(m * 4 + ks) * 32 + lane], al = Al[(m * 4 + ks) * 32 + lane];

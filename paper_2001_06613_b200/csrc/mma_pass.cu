@@ -38,12 +38,35 @@ static cudaError_t run_sample_then_gram(const Launch& L, const Args& a, float* V
   else k_sample_v<D, false, SPT, true><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  const long long ntiles = (npix + GMM::TP - 1) / GMM::TP;
+  const size_t stride = (size_t)GMM::KP * GMM::KP + 3 * GMM::KP;
+  EncodeTiledFn fn = encode_tiled_fn();
+  if (fn && !getenv("SEQREG_B200_GRAMREG")) {  // TMA-fed Gram (k_gram_tma)
+    CUtensorMap vmap;
+    memset(&vmap, 0, sizeof vmap);
+    cuuint64_t gdim[2] = {(cuuint64_t)npix, (cuuint64_t)a.K};
+    cuuint64_t gstr[1] = {(cuuint64_t)vstride * 4};
+    cuuint32_t box[2] = {(cuuint32_t)GTM::BOXP, (cuuint32_t)GTM::KP};
+    cuuint32_t es[2] = {1, 1};
+    if (fn(&vmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, V, gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+        CUDA_SUCCESS) {
+      const size_t smem = gtm_smem();
+      e = cudaFuncSetAttribute(k_gram_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      int grid = occupancy_grid(L, k_gram_tma, GTM::NT, smem, ntiles);
+      if ((size_t)grid * stride > part_cap) grid = (int)(part_cap / stride);
+      Args b = a;
+      b.part = part;
+      k_gram_tma<<<grid, GTM::NT, smem, L.stream>>>(b, vmap);
+      *nblk = grid;
+      return cudaGetLastError();
+    }
+  }
   const size_t smem = 4 * (size_t)GMM::KP * GMM::LD * sizeof(float);
   e = cudaFuncSetAttribute(k_gram_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const long long ntiles = (npix + GMM::TP - 1) / GMM::TP;
   int grid = occupancy_grid(L, k_gram_mma, GMM::NT, smem, ntiles);
-  const size_t stride = (size_t)GMM::KP * GMM::KP + 3 * GMM::KP;
   if ((size_t)grid * stride > part_cap) grid = (int)(part_cap / stride);
   Args b = a;
   b.part = part;
