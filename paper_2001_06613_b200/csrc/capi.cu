@@ -45,6 +45,7 @@ struct sr_ctx {
   int tex_enabled = 0;  // SEQREG_B200_TEX=1: texture-gather sampling (measured slower on B200)
   int tc = 1;      // SEQREG_B200_TC=0: SIMT Gram instead of tcgen05 in pass 1
   int tc2 = 0;     // SEQREG_B200_TC2=1: tcgen05 pass 2
+  int graphs = 1;  // SEQREG_B200_GRAPH=0: sr_evaluate launches its kernels one by one (no graph replay)
   int mma = 1;     // SEQREG_B200_MMA: 1 = k_sample_v + k_gram_mma + k_pass2_mma, 2 = fused k_sample_gram,
                    // 0 = k_sample_v + k_gram_tc (tcgen05) + k_pass2_stream
   int split = 1;   // SEQREG_B200_SPLIT=0: fused tensor-core pass 1 instead of sampling kernel + Gram kernel
@@ -67,6 +68,21 @@ struct sr_ctx {
     sr::NgfBufs ngf{};  // the split NGF path's buffers and ranges (feature == SR_NGF)
     int frame_index[SR_MAX_FRAMES];
   } vtag;
+  // One captured sr_evaluate (CUDA graph): the problem, weights and buffers it was captured for, its own
+  // device copy of the per-call constants (Job), the scratch epoch it is valid in, and what the sample
+  // buffers hold after it ran (restored into vtag on every replay).
+  struct EvalGraph {
+    std::vector<unsigned char> key;
+    cudaGraphExec_t exec = nullptr;
+    Job* job = nullptr;
+    unsigned long long epoch = 0;
+    unsigned long long last_use = 0;
+    int seen = 0;  // evaluations of this key so far (captured on the second)
+    VTag vt;
+  };
+  std::vector<EvalGraph> egraphs;
+  unsigned long long graph_clock = 0;
+  cudaStream_t cap_stream = nullptr;  // capture stream of the evaluation graphs
   Job* job_dev = nullptr;
   Job* job_host = nullptr;  // pinned staging
   Job job_last{};           // content of the last upload (skip identical re-uploads)
@@ -163,8 +179,13 @@ static int check_grid(const sr_grid& g) {
   return SR_OK;
 }
 
+// bumped by every scratch (re)allocation: a captured evaluation graph embeds scratch pointers and is
+// dropped once the epoch it was captured in has passed
+static unsigned long long g_alloc_epoch = 0;
+
 static int ensure(void** p, size_t* cap, size_t need_bytes) {
   if (*cap >= need_bytes) return SR_OK;
+  ++g_alloc_epoch;
   if (*p) cudaFree(*p);
   *p = nullptr;
   *cap = 0;
@@ -234,8 +255,8 @@ static Args make_args(sr_ctx* ctx, const sr_problem* p) {
 // Stage the per-call constants (frame indices, weights, affine rows) and upload them
 // when they differ from the last upload.  Identical constants cost nothing, which keeps
 // repeated evaluations (and CUDA-graph capture of them) free of host synchronisation.
-static int upload_job(sr_ctx* ctx, const sr_problem* p, const double* weights) {
-  Job nj = ctx->job_last;
+static void build_job(sr_ctx* ctx, const sr_problem* p, const double* weights, Job& nj) {
+  nj = ctx->job_last;
   for (int j = 0; j < p->k; ++j) {
     nj.frame_index[j] = p->frame_index[j];
     if (weights) nj.weights[j] = weights[j];
@@ -252,6 +273,11 @@ static int upload_job(sr_ctx* ctx, const sr_problem* p, const double* weights) {
     ctx->job_use_tex = ts != nullptr;
     for (int j = 0; j < p->k; ++j) nj.tex[j] = ts ? (unsigned long long)ts->tex[p->frame_index[j]] : 0ull;
   }
+}
+
+static int upload_job(sr_ctx* ctx, const sr_problem* p, const double* weights) {
+  Job nj;
+  build_job(ctx, p, weights, nj);
   if (ctx->job_valid && std::memcmp(&nj, &ctx->job_last, sizeof(Job)) == 0) return SR_OK;
   // the previous upload may still be in flight from the pinned staging buffer
   CK(cudaStreamSynchronize(ctx->stream));
@@ -496,6 +522,8 @@ int sr_create(int32_t device, sr_ctx** out) {
     c->p2s = (ps && ps[0] == '0') ? 0 : 1;
     const char* t2 = getenv("SEQREG_B200_TC2");
     c->tc2 = (t2 && t2[0] == '1') ? 1 : 0;
+    const char* gr = getenv("SEQREG_B200_GRAPH");
+    c->graphs = (gr && gr[0] == '0') ? 0 : 1;
     const char* mm = getenv("SEQREG_B200_MMA");
     c->mma = mm ? atoi(mm) : 1;
   }
@@ -524,6 +552,11 @@ int sr_destroy(sr_ctx* c) {
   cudaFree(c->zbuf);
   cudaFree(c->aux);
   cudaFree(c->iaux);
+  for (auto& eg : c->egraphs) {
+    if (eg.exec) cudaGraphExecDestroy(eg.exec);
+    cudaFree(eg.job);
+  }
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   delete c;
   return SR_OK;
 }
@@ -738,6 +771,38 @@ int sr_grad(sr_ctx* c, const sr_problem* p, const double* stats_dev, void* grad_
   return grad_impl(c, p, stats_dev, grad_dev, g_off, g_stride, c->sample_reuse != 0);
 }
 
+static int evaluate_impl(sr_ctx* c, const sr_problem* p, double cell_volume, double* raw_dev, double* stats_dev,
+                         void* grad_dev) {
+  int rc = corr_partial_impl(c, p, raw_dev, cell_volume, stats_dev);
+  if (rc) return rc;
+  if (!grad_dev) return SR_OK;
+  return grad_impl(c, p, stats_dev, grad_dev, p->y_off, p->param == SR_DISPLACEMENT ? p->y_stride : 0, true);
+}
+
+// Everything an evaluation's launches depend on: the problem's scalars and device pointers, the subset,
+// weights, affine parameters, cell volume and output buffers (the scratch pointers are covered by the
+// allocation epoch).
+static std::vector<unsigned char> eval_key(const sr_problem* p, const double* weights, double cell_volume,
+                                           const double* raw_dev, const double* stats_dev, const void* grad_dev) {
+  std::vector<unsigned char> k;
+  auto put = [&](const void* v, size_t n) {
+    const unsigned char* b = static_cast<const unsigned char*>(v);
+    k.insert(k.end(), b, b + n);
+  };
+  sr_problem q = *p;
+  q.frame_index = nullptr;
+  q.affine = nullptr;
+  put(&q, sizeof q);
+  put(p->frame_index, sizeof(int32_t) * p->k);
+  put(weights, sizeof(double) * p->k);
+  if (p->param == SR_AFFINE) put(p->affine, sizeof(double) * p->k * (p->grid.ndim * p->grid.ndim + p->grid.ndim));
+  put(&cell_volume, sizeof cell_volume);
+  put(&raw_dev, sizeof raw_dev);
+  put(&stats_dev, sizeof stats_dev);
+  put(&grad_dev, sizeof grad_dev);
+  return k;
+}
+
 int sr_evaluate(sr_ctx* c, const sr_problem* p, const double* weights, double cell_volume,
                 double* raw_dev, double* stats_dev, void* grad_dev) {
   int rc = check_problem(c, p);
@@ -746,12 +811,89 @@ int sr_evaluate(sr_ctx* c, const sr_problem* p, const double* weights, double ce
   const Geo g = make_geo(p->grid);
   if (p->pix_lo != 0 || p->pix_hi != g.N) return fail(SR_ERR_ARG, "sr_evaluate covers the whole grid");
   CK(cudaSetDevice(c->device));
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CK(cudaStreamIsCapturing(c->stream, &cs));
+  if (!c->graphs || c->tex_enabled || cs != cudaStreamCaptureStatusNone) {  // (the caller may be capturing)
+    rc = upload_job(c, p, weights);
+    if (rc) return rc;
+    return evaluate_impl(c, p, cell_volume, raw_dev, stats_dev, grad_dev);
+  }
+  // CUDA-graph replay of a repeated evaluation (the objective inside an optimiser loop): one graph
+  // launch instead of the per-kernel launches.  A key is captured on its second evaluation (the first
+  // runs eagerly and sizes every scratch buffer); the graph reads its own device copy of the Job.
+  const std::vector<unsigned char> key = eval_key(p, weights, cell_volume, raw_dev, stats_dev, grad_dev);
+  sr_ctx::EvalGraph* eg = nullptr;
+  for (auto& e : c->egraphs)
+    if (e.key == key) eg = &e;
+  if (eg && eg->exec && eg->epoch != g_alloc_epoch) {  // scratch moved since the capture
+    cudaGraphExecDestroy(eg->exec);
+    eg->exec = nullptr;
+    eg->seen = 0;
+  }
+  if (eg && eg->exec) {
+    eg->last_use = ++c->graph_clock;
+    c->vtag = eg->vt;
+    CK(cudaGraphLaunch(eg->exec, c->stream));
+    return SR_OK;
+  }
+  if (!eg) {
+    if (c->egraphs.size() >= 8) {  // replace the least recently used entry
+      auto lru = std::min_element(c->egraphs.begin(), c->egraphs.end(),
+                                  [](const sr_ctx::EvalGraph& x, const sr_ctx::EvalGraph& y) {
+                                    return x.last_use < y.last_use;
+                                  });
+      if (lru->exec) cudaGraphExecDestroy(lru->exec);
+      cudaFree(lru->job);
+      c->egraphs.erase(lru);
+    }
+    c->egraphs.push_back(sr_ctx::EvalGraph{});
+    eg = &c->egraphs.back();
+    eg->key = key;
+  }
+  eg->last_use = ++c->graph_clock;
+  if (eg->seen++ == 0) {  // first evaluation of this key: eager
+    rc = upload_job(c, p, weights);
+    if (rc) return rc;
+    return evaluate_impl(c, p, cell_volume, raw_dev, stats_dev, grad_dev);
+  }
+  // second evaluation: capture (scratch is sized by the eager run), then launch
+  Job nj;
+  build_job(c, p, weights, nj);
+  if (!eg->job) CK(cudaMalloc(&eg->job, sizeof(Job)));
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaMemcpy(eg->job, &nj, sizeof(Job), cudaMemcpyHostToDevice));
+  const unsigned long long epoch = g_alloc_epoch;
+  Job* saved = c->job_dev;
+  c->job_dev = eg->job;
+  // capture on a private stream (the legacy default stream cannot be captured); the graph is then
+  // launched into the context's stream
+  if (!c->cap_stream) CK(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+  const cudaStream_t user_stream = c->stream;
+  c->stream = c->cap_stream;
+  cudaGraph_t graph = nullptr;
+  cudaError_t be = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal);
+  rc = be == cudaSuccess ? evaluate_impl(c, p, cell_volume, raw_dev, stats_dev, grad_dev) : SR_OK;
+  const cudaError_t ce = be == cudaSuccess ? cudaStreamEndCapture(c->stream, &graph) : be;
+  c->stream = user_stream;
+  c->job_dev = saved;
+  if (rc == SR_OK && ce == cudaSuccess && epoch == g_alloc_epoch) {
+    const cudaError_t ie = cudaGraphInstantiate(&eg->exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ie == cudaSuccess) {
+      eg->epoch = epoch;
+      eg->vt = c->vtag;
+      CK(cudaGraphLaunch(eg->exec, c->stream));
+      return SR_OK;
+    }
+    eg->exec = nullptr;
+  } else if (graph) {
+    cudaGraphDestroy(graph);
+  }
+  cudaGetLastError();  // clear a capture error; fall back to the eager path for this call
+  c->graphs = 0;       // and for the rest of this context's life
   rc = upload_job(c, p, weights);
   if (rc) return rc;
-  rc = corr_partial_impl(c, p, raw_dev, cell_volume, stats_dev);
-  if (rc) return rc;
-  if (!grad_dev) return SR_OK;
-  return grad_impl(c, p, stats_dev, grad_dev, p->y_off, p->param == SR_DISPLACEMENT ? p->y_stride : 0, true);
+  return evaluate_impl(c, p, cell_volume, raw_dev, stats_dev, grad_dev);
 }
 
 int sr_curvature(sr_ctx* c, const sr_problem* p, double alpha, double h, void* grad, int64_t g_off,

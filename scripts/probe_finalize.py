@@ -64,6 +64,23 @@ def main():
     print(f"finalize only (k_finalize): {timed(lambda: plan.finalize(prob, w, grid.cell_volume)):.2f} us")
     print(f"corr_partial (pass 1 + reduce): {timed(lambda: plan.corr_partial(prob)):.2f} us")
     print(f"evaluate: {timed(lambda: plan.evaluate(prob, w, grid.cell_volume, g)):.2f} us")
+    import time
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.reps):
+        plan.evaluate(prob, w, grid.cell_volume, g)
+    t1 = time.perf_counter()
+    torch.cuda.synchronize()
+    print(f"host enqueue per evaluate: {(t1 - t0) / args.reps * 1e6:.2f} us")
+    gr = torch.cuda.CUDAGraph()
+    s2 = torch.cuda.Stream()
+    with torch.cuda.stream(s2):
+        plan.evaluate(prob, w, grid.cell_volume, g)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(gr, stream=s2):
+            plan.evaluate(prob, w, grid.cell_volume, g)
+    torch.cuda.synchronize()
+    print(f"graph replay: {timed(lambda: gr.replay()):.2f} us")
 
 
 if __name__ == "__main__":

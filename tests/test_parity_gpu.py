@@ -306,6 +306,34 @@ def test_deterministic_bitwise():
     assert torch.equal(s1, s2) and torch.equal(g1, g2)
 
 
+@pytest.mark.parametrize("feature", ["ncc", "ngf"])
+def test_graph_replay_matches_eager(feature):
+    """sr_evaluate captures a repeated evaluation as a CUDA graph (2nd call) and replays it (3rd+):
+    bitwise the eager result on the same y, and the oracle's after y is rewritten in place."""
+    rng = np.random.default_rng(11)
+    dims, K = (40, 36), 24
+    frames, spacing, origin, y, w = _random_problem(rng, dims, K)
+    fd = _frames_dev(frames, dims, spacing, origin, torch.float32)
+    h = float(np.prod(spacing))
+    obj = srb.FieldObjective(fd, list(range(K)), w, h, feature=feature, ngf_eps=0.2)
+    yt = torch.as_tensor(y, dtype=torch.float32, device=fd.data.device).contiguous()
+    g = torch.empty_like(yt)
+    outs = []
+    for _ in range(3):  # eager, capture + launch, replay
+        s, _ = obj.evaluate(yt, g)
+        outs.append((s.clone(), g.clone()))
+    for s, gg in outs[1:]:
+        assert torch.equal(s[:4], outs[0][0][:4]) and torch.equal(gg, outs[0][1])
+    y2 = y + 0.1 * rng.standard_normal(y.shape) * np.asarray(spacing)[None, :, None]
+    yt.copy_(torch.as_tensor(y2, dtype=torch.float32))
+    s, _ = obj.evaluate(yt, g)  # replay on new contents
+    q = frames.astype(np.float32).astype(np.float64)
+    yq = yt.double().cpu().numpy()
+    _, Dref, gref = orc.evaluate_field(list(q), dims, spacing, origin, yq, w, h, feature, 0.2)
+    assert float(s[0].item()) == pytest.approx(Dref, rel=1e-4)
+    assert _relmax(g.double().cpu().numpy(), gref) < 1e-4
+
+
 def test_degenerate_and_outside_fields():
     """A frame warped entirely outside the hull is constant (0): degenerate, zero C row and
     zero gradient, exactly like the reference's zero feature vector (similarity.py:84-86)."""

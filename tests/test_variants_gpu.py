@@ -6,6 +6,7 @@ oracle's D and dD/dy: each variant runs the fp32 field parity cases in a fresh p
     SEQREG_B200_TC2=1     tcgen05 pass 2 (2-D)
     SEQREG_B200_P2S=0     re-gathering pass 2 (default: streaming pass 2 from the split pass 1's V, grad T)
     SEQREG_B200_SPLIT=0   fused tcgen05 pass 1 (default: sampling kernel + tcgen05 Gram kernel)
+    SEQREG_B200_GRAPH=0   no CUDA-graph replay of repeated sr_evaluate calls
     SEQREG_B200_MMA=0     k_sample_v + k_gram_tc + k_pass2_stream (default: k_sample_gram + k_pass2_mma)
     SEQREG_B200_WS2=1     warp-specialized SIMT pass 2
 """
@@ -63,7 +64,7 @@ print(json.dumps(out))
 
 
 @pytest.mark.parametrize("env", ["SEQREG_B200_LEGACY=1", "SEQREG_B200_TC=0", "SEQREG_B200_TC2=1", "SEQREG_B200_P2S=0",
-                                 "SEQREG_B200_SPLIT=0", "SEQREG_B200_WS2=1", "SEQREG_B200_MMA=0", ""])
+                                 "SEQREG_B200_SPLIT=0", "SEQREG_B200_WS2=1", "SEQREG_B200_MMA=0", "SEQREG_B200_GRAPH=0", ""])
 def test_variant_parity(env):
     e = dict(os.environ)
     if env:
