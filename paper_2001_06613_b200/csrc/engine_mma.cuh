@@ -628,11 +628,11 @@ __global__ void __launch_bounds__(GTM::NT, 2) k_gram_tma(const Args a, const __g
 // with coalesced 128-bit loads and a stmatrix epilogue (48.6 us: two exposed latencies per block at 24
 // warps/SM), and the same math fed by per-warp two-stage 1-D bulk-copy pipelines (k_pass2_bulk, 41.8 us).
 struct P2M {
-  static constexpr int KP = 32, NT = 256, PW = 8;
+  static constexpr int KP = 32, NT = 256, PW = 16;
 };
 
-template <int D>
-__global__ void __launch_bounds__(P2M::NT, 3) k_pass2_mma(const Args a, const float* __restrict__ V,
+template <int D, int MINB>
+__global__ void __launch_bounds__(P2M::NT, MINB) k_pass2_mma(const Args a, const float* __restrict__ V,
                                                           const float* __restrict__ G, long long vstride) {
   // A fragments: [mtile 2][kstep 4][lane 32] x {hi a0..a3} and {lo a0..a3}
   __shared__ __align__(16) float4 Ah[2 * 4 * 32], Al[2 * 4 * 32];
@@ -670,23 +670,30 @@ __global__ void __launch_bounds__(P2M::NT, 3) k_pass2_mma(const Args a, const fl
   const int vs = (int)vstride, os = (int)a.o_stride;
   const uint64_t pol = l2_policy_evict_first();
   float* __restrict__ ob = reinterpret_cast<float*>(a.out) + (a.pix_lo - a.o_off);
-  const bool vec_out = ((reinterpret_cast<uintptr_t>(ob) | (uintptr_t)os) & 1) == 0;  // float2 stores aligned
+  // 128-bit accesses need 16-byte aligned rows (else the scalar paths)
+  const bool vin = (vs & 3) == 0 && (reinterpret_cast<uintptr_t>(G) & 15) == 0;
+  const bool vout = (os & 3) == 0 && (reinterpret_cast<uintptr_t>(ob) & 15) == 0;
   for (int blk = blockIdx.x * (P2M::NT / 32) + warp; blk < nblk; blk += gridDim.x * (P2M::NT / 32)) {
     const int p0 = blk * P2M::PW;
     const bool fullb = p0 + P2M::PW <= npix;
-    // B fragments: b0 = V[8 ks + t][p0 + g], b1 = V[8 ks + t + 4][p0 + g]
-    const int pg = p0 + g;
-    const bool okg = pg < npix;
-    float bv[4][2];
+    // B column g of n-tile nt carries pixel 4 (g >> 1) + 2 nt + (g & 1), so that the C fragments of a
+    // lane (columns 2t, 2t + 1 of both n-tiles) are the 4 consecutive pixels p0 + 4t .. p0 + 4t + 3
+    float bv[4][2][2];  // [ks][nt][u]: V[8 ks + t + 4 u][p0 + pixel(g, nt)]
 #pragma unroll
-    for (int ks = 0; ks < 4; ++ks) {
-      const int i0 = 8 * ks + t, i1 = i0 + 4;
-      bv[ks][0] = (i0 < K && okg) ? ldg_hint_nv(V + (i0 * vs + pg), pol) : 0.f;
-      bv[ks][1] = (i1 < K && okg) ? ldg_hint_nv(V + (i1 * vs + pg), pol) : 0.f;
+    for (int nt = 0; nt < 2; ++nt) {
+      const int pg = p0 + 4 * (g >> 1) + 2 * nt + (g & 1);
+      const bool okg = pg < npix;
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int i = 8 * ks + t + 4 * u;
+          bv[ks][nt][u] = (i < K && okg) ? ldg_hint_nv(V + (i * vs + pg), pol) : 0.f;
+        }
     }
-    // grad T of this lane's outputs (frames 16 m + g + 8 h, pixels p0 + 2t, p0 + 2t + 1)
-    const int pq = p0 + 2 * t;
-    float2 gv[2][2][D];
+    // grad T of this lane's outputs: frames 16 m + g + 8 h, pixels p0 + 4t .. + 3 (one 128-bit load)
+    const int pq = p0 + 4 * t;
+    float4 gv[2][2][D];
 #pragma unroll
     for (int m = 0; m < 2; ++m)
 #pragma unroll
@@ -695,26 +702,34 @@ __global__ void __launch_bounds__(P2M::NT, 3) k_pass2_mma(const Args a, const fl
 #pragma unroll
         for (int c = 0; c < D; ++c) {
           const float* src = G + ((j * D + c) * vs + pq);
-          if (fullb) {
-            gv[m][h][c] = __ldcs(reinterpret_cast<const float2*>(src));
+          if (fullb && vin) {
+            gv[m][h][c] = __ldcs(reinterpret_cast<const float4*>(src));
           } else {
             gv[m][h][c].x = pq < npix ? src[0] : 0.f;
             gv[m][h][c].y = pq + 1 < npix ? src[1] : 0.f;
+            gv[m][h][c].z = pq + 2 < npix ? src[2] : 0.f;
+            gv[m][h][c].w = pq + 3 < npix ? src[3] : 0.f;
           }
         }
       }
-    float acc[2][4], ac1[2][4] = {}, ac2[2][4] = {};  // HH (+ beta'), LH, HL chains
+    float acc[2][2][4];  // [m][nt]: four independent accumulator chains (beta' + HH + LH + HL)
 #pragma unroll
-    for (int m = 0; m < 2; ++m) {
-      acc[m][0] = acc[m][1] = bet[m][0];
-      acc[m][2] = acc[m][3] = bet[m][1];
-    }
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        acc[m][nt][0] = acc[m][nt][1] = bet[m][0];
+        acc[m][nt][2] = acc[m][nt][3] = bet[m][1];
+      }
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks) {
-      // hi by truncation (exact in tf32, one LOP3), lo = v - hi exactly (see split_q)
-      const uint32_t bh0 = __float_as_uint(bv[ks][0]) & 0xffffe000u, bh1 = __float_as_uint(bv[ks][1]) & 0xffffe000u;
-      const uint32_t bl0 = __float_as_uint(bv[ks][0] - __uint_as_float(bh0));
-      const uint32_t bl1 = __float_as_uint(bv[ks][1] - __uint_as_float(bh1));
+      uint32_t bh[2][2], bl[2][2];
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {  // hi by truncation (exact in tf32), lo = v - hi exactly (see split_q)
+          bh[nt][u] = __float_as_uint(bv[ks][nt][u]) & 0xffffe000u;
+          bl[nt][u] = __float_as_uint(bv[ks][nt][u] - __uint_as_float(bh[nt][u]));
+        }
 #pragma unroll
       for (int m = 0; m < 2; ++m) {
         const float4 ah = Ah[(m * 4 + ks) * 32 + lane], al = Al[(m * 4 + ks) * 32 + lane];
@@ -722,31 +737,35 @@ __global__ void __launch_bounds__(P2M::NT, 3) k_pass2_mma(const Args a, const fl
                                 __float_as_uint(ah.w)};
         const uint32_t AL[4] = {__float_as_uint(al.x), __float_as_uint(al.y), __float_as_uint(al.z),
                                 __float_as_uint(al.w)};
-        mma_tf32(acc[m], AH, bh0, bh1);
-        mma_tf32(ac1[m], AL, bh0, bh1);
-        mma_tf32(ac2[m], AH, bl0, bl1);
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          mma_tf32(acc[m][nt], AH, bh[nt][0], bh[nt][1]);
+          mma_tf32(acc[m][nt], AL, bh[nt][0], bh[nt][1]);
+          mma_tf32(acc[m][nt], AH, bl[nt][0], bl[nt][1]);
+        }
       }
     }
-#pragma unroll
-    for (int m = 0; m < 2; ++m)
-#pragma unroll
-      for (int r = 0; r < 4; ++r) acc[m][r] += ac1[m][r] + ac2[m][r];
-    // epilogue: acc[m][2h + u] = q_j(p0 + 2t + u), j = 16 m + g + 8 h
+    // epilogue: acc[m][nt][2h + u] = q_j(p0 + 4t + 2 nt + u), j = 16 m + g + 8 h; one 128-bit store per (j, c)
 #pragma unroll
     for (int m = 0; m < 2; ++m)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int j = 16 * m + g + 8 * h;
         if (j < K) {
+          const float q0 = acc[m][0][2 * h], q1 = acc[m][0][2 * h + 1];
+          const float q2 = acc[m][1][2 * h], q3 = acc[m][1][2 * h + 1];
 #pragma unroll
           for (int c = 0; c < D; ++c) {
             float* dst = ob + ((j * D + c) * os + pq);
-            const float2 r = make_float2(acc[m][2 * h] * gv[m][h][c].x, acc[m][2 * h + 1] * gv[m][h][c].y);
-            if (fullb && vec_out) {
-              __stcs(reinterpret_cast<float2*>(dst), r);
+            const float4 gg = gv[m][h][c];
+            const float4 r = make_float4(q0 * gg.x, q1 * gg.y, q2 * gg.z, q3 * gg.w);
+            if (fullb && vout) {
+              __stcs(reinterpret_cast<float4*>(dst), r);
             } else {
               if (pq < npix) __stcs(dst, r.x);
               if (pq + 1 < npix) __stcs(dst + 1, r.y);
+              if (pq + 2 < npix) __stcs(dst + 2, r.z);
+              if (pq + 3 < npix) __stcs(dst + 3, r.w);
             }
           }
         }

@@ -93,8 +93,11 @@ static cudaError_t run_pass2_mma(const Launch& L, const Args& a, const float* V,
   }
   const long long nblk = (npix + P2M::PW - 1) / P2M::PW;
   const long long want = (nblk + P2M::NT / 32 - 1) / (P2M::NT / 32);
-  const int grid = occupancy_grid(L, k_pass2_mma<D>, P2M::NT, 0, want);
-  k_pass2_mma<D><<<grid, P2M::NT, 0, L.stream>>>(a, V, G, vstride);
+  // SEQREG_B200_P2B: minimum resident CTAs per SM the pass-2 kernel is compiled for (register budget)
+  static const int minb = getenv("SEQREG_B200_P2B") ? atoi(getenv("SEQREG_B200_P2B")) : 2;
+  auto kern = minb == 3 ? k_pass2_mma<D, 3> : k_pass2_mma<D, 2>;
+  const int grid = occupancy_grid(L, kern, P2M::NT, 0, want);
+  kern<<<grid, P2M::NT, 0, L.stream>>>(a, V, G, vstride);
   return cudaGetLastError();
 }
 
