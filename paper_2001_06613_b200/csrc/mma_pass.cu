@@ -32,10 +32,22 @@ static cudaError_t run_sample_then_gram(const Launch& L, const Args& a, float* V
                                         double* part, size_t part_cap, int* nblk) {
   const long long npix = a.pix_hi - a.pix_lo;
   if (npix <= 0 || a.K > GMM::KP) return cudaErrorInvalidValue;
-  constexpr int SPT = 4;
-  const dim3 sgrid((unsigned)((npix + 256 * SPT - 1) / (256 * SPT)), (unsigned)a.K);
-  if (a.g.pow2) k_sample_v<D, true, SPT, true><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
-  else k_sample_v<D, false, SPT, true><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
+  // SEQREG_B200_SPT: samples in flight per thread of k_sample_v (2, 4 or 8)
+  static const int spt = getenv("SEQREG_B200_SPT") ? atoi(getenv("SEQREG_B200_SPT")) : 4;
+  if (spt == 8) {
+    const dim3 sgrid((unsigned)((npix + 256 * 8 - 1) / (256 * 8)), (unsigned)a.K);
+    if (a.g.pow2) k_sample_v<D, true, 8, true><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
+    else k_sample_v<D, false, 8, true><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
+  } else if (spt == 2) {
+    const dim3 sgrid((unsigned)((npix + 256 * 2 - 1) / (256 * 2)), (unsigned)a.K);
+    if (a.g.pow2) k_sample_v<D, true, 2, true><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
+    else k_sample_v<D, false, 2, true><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
+  } else {
+    constexpr int SPT = 4;
+    const dim3 sgrid((unsigned)((npix + 256 * SPT - 1) / (256 * SPT)), (unsigned)a.K);
+    if (a.g.pow2) k_sample_v<D, true, SPT, true><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
+    else k_sample_v<D, false, SPT, true><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const long long ntiles = (npix + GMM::TP - 1) / GMM::TP;
