@@ -304,10 +304,21 @@ static cudaError_t launch_reduce_finalize(sr_ctx* c, const sr_problem* p, int nb
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(dsm, 1));
   if (e != cudaSuccess) return e;
   const int stride = KP * KP + 3 * KP;
-  kern<<<(stride + 31) / 32, 1024, dsm, c->stream>>>(c->part, nblk, KP, p->k, count, raw, do_final, c->job_dev,
-                                                      p->feature, p->grid.ndim, h, (const T*)p->shifts_dev,
-                                                      stats, c->ticket);
-  return cudaGetLastError();
+  // PDL (SEQREG_B200_PDL=1, off by default: measured slower): may start while pass 1 drains
+  static const bool pdl = getenv("SEQREG_B200_PDL") && getenv("SEQREG_B200_PDL")[0] == '1';
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((stride + 31) / 32);
+  cfg.blockDim = dim3(1024);
+  cfg.dynamicSmemBytes = dsm;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, (const double*)c->part, nblk, KP, (int)p->k, count, raw, do_final,
+                            (const Job*)c->job_dev, (int)p->feature, (int)p->grid.ndim, h, (const T*)p->shifts_dev,
+                            stats, c->ticket);
 }
 
 // pass 1 over the slab, then the fixed-order cross-CTA reduction into raw (and, with

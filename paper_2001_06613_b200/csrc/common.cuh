@@ -102,6 +102,12 @@ __device__ __forceinline__ void stg4_hint(float* p, float4 v, uint64_t pol) {
                : "memory");
 }
 
+// Programmatic dependent launch (PDL): a dependent kernel launched with programmatic stream
+// serialization may start while its predecessor drains; it must wait before touching the
+// predecessor's results (a no-op when launched normally).  The predecessor lets it launch early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 // Cell-centre world coordinate o + (i + 0.5) * s, rounded like numpy
 // (grid.py:172-177: origin + (arange + 0.5) * spacing).
 __device__ __forceinline__ double center(const Geo& g, int a, int i) {

@@ -795,6 +795,8 @@ __global__ void __launch_bounds__(1024) k_reduce_finalize(const double* __restri
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ double buf[32][33];
   __shared__ int is_last;
+  pdl_wait();     // the pass-1 partials
+  pdl_trigger();  // pass 2 may be scheduled now (it waits for this grid's completion itself)
   const int stride = KP * KP + 3 * KP;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int e = blockIdx.x * 32 + lane;

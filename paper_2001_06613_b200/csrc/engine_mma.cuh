@@ -447,6 +447,8 @@ __global__ void __launch_bounds__(GTM::NT, 2) k_gram_tma(const Args a, const __g
     fence_mbar_init();
     tma_prefetch_desc(&vmap);
   }
+  pdl_wait();  // V of the sampling kernel
+  pdl_trigger();
   __syncthreads();
   auto issue = [&](long long n, int s2) {
     const int x0 = (int)((blockIdx.x + n * gridDim.x) * TP);
@@ -641,6 +643,7 @@ __global__ void __launch_bounds__(P2M::NT, MINB) k_pass2_mma(const Args a, const
   const int K = a.K;
   const StatsLayout L(K);
   const double* Md = a.stats + L.M;
+  pdl_wait();  // M', beta' of the finalize
   for (int e = tid; e < 2 * 4 * 32; e += P2M::NT) {
     const int m = e >> 7, ks = (e >> 5) & 3, ln = e & 31;
     const int gg = ln >> 2, tt = ln & 3;

@@ -274,6 +274,7 @@ __global__ void __launch_bounds__(256, 8) k_sample_v(const Args a, float* __rest
                                                      long long vstride) {
   // grid (pixel blocks, K): block-uniform 64-bit bases, 32-bit per-thread offsets
   constexpr int BP = 256 * SPT;  // pixels per block
+  if (GV) pdl_trigger();  // the Gram kernel may be scheduled as this grid's last wave starts
   const int npix = (int)(a.pix_hi - a.pix_lo);
   const int k = (int)blockIdx.y;
   const int b0 = (int)blockIdx.x * BP;

@@ -1,10 +1,30 @@
 // Launchers for engine_mma.cuh (fp32 NCC displacement fields, K <= 32, 2-D and 3-D).
 #include <cstdio>
 #include <cstdlib>
+#include <utility>
 #include "engine_mma.cuh"
 #include "launch.cuh"
 
 namespace sr {
+
+// launch with programmatic stream serialization (PDL) when SEQREG_B200_PDL=1 (measured slower at C2:
+// 95.3 vs 91.1 us per step — early-resident dependent CTAs take slots from the draining predecessor)
+template <typename... KArgs, typename... Args2>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args2&&... args) {
+  static const bool on = getenv("SEQREG_B200_PDL") && getenv("SEQREG_B200_PDL")[0] == '1';
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = on ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args2>(args)...);
+}
 
 template <int D>
 static cudaError_t run_sample_gram(const Launch& L, const Args& a, float* V, float* G, long long vstride,
@@ -70,9 +90,9 @@ static cudaError_t run_sample_then_gram(const Launch& L, const Args& a, float* V
       if ((size_t)grid * stride > part_cap) grid = (int)(part_cap / stride);
       Args b = a;
       b.part = part;
-      k_gram_tma<<<grid, GTM::NT, smem, L.stream>>>(b, vmap);
+      e = launch_pdl(k_gram_tma, dim3(grid), dim3(GTM::NT), smem, L.stream, b, vmap);
       *nblk = grid;
-      return cudaGetLastError();
+      return e;
     }
   }
   const size_t smem = 4 * (size_t)GMM::KP * GMM::LD * sizeof(float);
@@ -109,8 +129,7 @@ static cudaError_t run_pass2_mma(const Launch& L, const Args& a, const float* V,
   static const int minb = getenv("SEQREG_B200_P2B") ? atoi(getenv("SEQREG_B200_P2B")) : 2;
   auto kern = minb == 3 ? k_pass2_mma<D, 3> : k_pass2_mma<D, 2>;
   const int grid = occupancy_grid(L, kern, P2M::NT, 0, want);
-  kern<<<grid, P2M::NT, 0, L.stream>>>(a, V, G, vstride);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3(grid), dim3(P2M::NT), 0, L.stream, a, V, G, vstride);
 }
 
 cudaError_t sample_gram_d2(const Launch& L, const Args& a, float* V, float* G, long long vstride, double* part,
