@@ -947,4 +947,161 @@ __global__ void __launch_bounds__(P2B<D>::NT, 1) k_pass2_bulk(const Args a, cons
   // drain: no copies may be in flight when the CTA exits (every issued stage was waited on above)
 }
 
+// Split NGF pass 2, z = dD/d(grad u) on the tensor cores (fp32 displacement fields, K <= 128):
+//   R^T = M'^T N: A = M'^T (m = frame j, k = frame i; hi/lo fragments for every (m-tile, k-step) staged
+//   once per persistent CTA in shared memory), B = N (k = frame i, n = (component, pixel); fragments
+//   straight from global, each n element loaded once per warp item), 3xTF32, fp32 accumulation.
+//   B column g of the n-tile pair q of component c carries pixel 4 (g >> 1) + 2 q + (g & 1), so a lane
+//   owns 4 consecutive pixels of rows j = 16 m + g (+ 8) for every component: the epilogue
+//   z_(j,c) = (r_(j,c) - n_(j,c) sum_c' n_(j,c') r_(j,c')) / rho_j (the k_ngf_z arithmetic) reads n and
+//   rho and writes z with 128-bit accesses.
+// Work item = (16-pixel block of [zlo, zhi), group of MW m-tiles); warps stride over items.
+template <int D>
+struct NZ {
+  static constexpr int NT = 512, PW = 16, MW = D == 2 ? 4 : 2, NTL = 2 * D;  // n-tiles per item
+};
+
+template <int D>
+__global__ void __launch_bounds__(NZ<D>::NT, 1) k_ngf_z_mma(const Args a, const float* __restrict__ Nf,
+                                                           const float* __restrict__ Rho, long long zlo,
+                                                           long long zhi, long long zstride, float* __restrict__ Z) {
+  using C = NZ<D>;
+  constexpr int MW = C::MW, NTL = C::NTL, PW = C::PW;
+  extern __shared__ __align__(16) float4 nz_sh[];
+  const int K = a.K;
+  const int KS = (K + 7) / 8, JT = (K + 15) / 16;  // k-steps, m-tiles (frames padded with zeros)
+  float4* Ah = nz_sh;                // [JT][KS][32]
+  float4* Al = nz_sh + JT * KS * 32;  // lo
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const StatsLayout L(K);
+  const double* Md = a.stats + L.M;
+  for (int e = tid; e < JT * KS * 32; e += C::NT) {
+    const int m = e / (KS * 32), ks = (e / 32) % KS, ln = e & 31;
+    const int gg = ln >> 2, tt = ln & 3;
+    float hv[4], lv[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {  // a0 (g, t), a1 (g + 8, t), a2 (g, t + 4), a3 (g + 8, t + 4); A[j][i] = M'[i][j]
+      const int j = 16 * m + gg + 8 * (r & 1), i = 8 * ks + tt + 4 * (r >> 1);
+      const double mv = (i < K && j < K) ? Md[i * K + j] : 0.0;
+      hv[r] = to_tf32((float)mv);
+      lv[r] = (float)(mv - (double)hv[r]);
+    }
+    Ah[e] = make_float4(hv[0], hv[1], hv[2], hv[3]);
+    Al[e] = make_float4(lv[0], lv[1], lv[2], lv[3]);
+  }
+  __syncthreads();
+  const int nzp = (int)(zhi - zlo);  // z range (32-bit: the launcher checks K D zstride < 2^31)
+  const int zs = (int)zstride;
+  const int nblk = (nzp + PW - 1) / PW;
+  const int ngrp = (JT + MW - 1) / MW;
+  const bool vec = (zs & 3) == 0 && ((reinterpret_cast<uintptr_t>(Nf) | reinterpret_cast<uintptr_t>(Rho) |
+                                     reinterpret_cast<uintptr_t>(Z)) & 15) == 0;
+  for (int item = blockIdx.x * (C::NT / 32) + warp; item < nblk * ngrp; item += gridDim.x * (C::NT / 32)) {
+    const int blk = item / ngrp, m0 = (item % ngrp) * MW;
+    const int mc = min(MW, JT - m0);
+    const int p0 = blk * PW;
+    const bool fullb = p0 + PW <= nzp && vec;
+    float acc[MW][NTL][4];
+#pragma unroll
+    for (int m = 0; m < MW; ++m)
+#pragma unroll
+      for (int nt = 0; nt < NTL; ++nt)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[m][nt][r] = 0.f;
+    // pixel of B column g in the n-tile pair half q
+    int pq[2];
+    bool okq[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      pq[q] = p0 + 4 * (g >> 1) + 2 * q + (g & 1);
+      okq[q] = pq[q] < nzp;
+    }
+    for (int ks = 0; ks < KS; ++ks) {
+      uint32_t bh[NTL][2], bl[NTL][2];
+#pragma unroll
+      for (int nt = 0; nt < NTL; ++nt)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int i = 8 * ks + t + 4 * u, c = nt >> 1, q = nt & 1;
+          const float v = (i < K && okq[q]) ? __ldg(Nf + ((i * D + c) * zs + pq[q])) : 0.f;
+          bh[nt][u] = __float_as_uint(v) & 0xffffe000u;  // hi by truncation, lo exact (see split_q)
+          bl[nt][u] = __float_as_uint(v - __uint_as_float(bh[nt][u]));
+        }
+#pragma unroll
+      for (int m = 0; m < MW; ++m) {
+        if (m < mc) {
+          const float4 ah = Ah[((m0 + m) * KS + ks) * 32 + lane], al = Al[((m0 + m) * KS + ks) * 32 + lane];
+          const uint32_t AH[4] = {__float_as_uint(ah.x), __float_as_uint(ah.y), __float_as_uint(ah.z),
+                                  __float_as_uint(ah.w)};
+          const uint32_t AL[4] = {__float_as_uint(al.x), __float_as_uint(al.y), __float_as_uint(al.z),
+                                  __float_as_uint(al.w)};
+#pragma unroll
+          for (int nt = 0; nt < NTL; ++nt) {
+            mma_tf32(acc[m][nt], AH, bh[nt][0], bh[nt][1]);
+            mma_tf32(acc[m][nt], AL, bh[nt][0], bh[nt][1]);
+            mma_tf32(acc[m][nt], AH, bl[nt][0], bl[nt][1]);
+          }
+        }
+      }
+    }
+    // epilogue: rows j = 16 (m0 + m) + g + 8 h, pixels p0 + 4t .. + 3
+    const int pz = p0 + 4 * t;
+#pragma unroll
+    for (int m = 0; m < MW; ++m)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = 16 * (m0 + m) + g + 8 * h;
+        if (m < mc && j < K) {
+          float r[D][4], n[D][4], rho[4];
+#pragma unroll
+          for (int c = 0; c < D; ++c) {
+            r[c][0] = acc[m][2 * c][2 * h];
+            r[c][1] = acc[m][2 * c][2 * h + 1];
+            r[c][2] = acc[m][2 * c + 1][2 * h];
+            r[c][3] = acc[m][2 * c + 1][2 * h + 1];
+          }
+          if (fullb) {
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+              const float4 v = __ldg(reinterpret_cast<const float4*>(Nf + ((j * D + c) * zs + pz)));
+              n[c][0] = v.x, n[c][1] = v.y, n[c][2] = v.z, n[c][3] = v.w;
+            }
+            const float4 v = __ldg(reinterpret_cast<const float4*>(Rho + (j * zs + pz)));
+            rho[0] = v.x, rho[1] = v.y, rho[2] = v.z, rho[3] = v.w;
+          } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const bool ok = pz + u < nzp;
+#pragma unroll
+              for (int c = 0; c < D; ++c) n[c][u] = ok ? Nf[(j * D + c) * zs + pz + u] : 0.f;
+              rho[u] = ok ? Rho[j * zs + pz + u] : 1.f;
+            }
+          }
+          float zz[D][4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            float dot = 0.f;
+#pragma unroll
+            for (int c = 0; c < D; ++c) dot += n[c][u] * r[c][u];
+            const float ir = 1.f / rho[u];
+#pragma unroll
+            for (int c = 0; c < D; ++c) zz[c][u] = (r[c][u] - n[c][u] * dot) * ir;
+          }
+#pragma unroll
+          for (int c = 0; c < D; ++c) {
+            float* dst = Z + ((j * D + c) * zs + pz);
+            if (fullb) {
+              *reinterpret_cast<float4*>(dst) = make_float4(zz[c][0], zz[c][1], zz[c][2], zz[c][3]);
+            } else {
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (pz + u < nzp) dst[u] = zz[c][u];
+            }
+          }
+        }
+      }
+  }
+}
+
 }  // namespace sr

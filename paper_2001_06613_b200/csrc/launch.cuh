@@ -349,9 +349,21 @@ cudaError_t run_ngf_pass1(const Launch& L, const Args& a, const NgfBufs& B, doub
                    : run_ngf_pass1_kp<D, 128>(L, a, B, part, part_cap, nblk);
 }
 
+cudaError_t ngf_z_mma_d2(const Launch& L, const Args& a, const NgfBufs& B);
+cudaError_t ngf_z_mma_d3(const Launch& L, const Args& a, const NgfBufs& B);
+
 template <int D>
 cudaError_t run_ngf_pass2(const Launch& L, const Args& a, const NgfBufs& B) {
   const int K = a.K;
+  static const bool zmma = !(getenv("SEQREG_B200_NGFZ") && getenv("SEQREG_B200_NGFZ")[0] == '0');
+  cudaError_t ez = cudaErrorNotSupported;
+  if (zmma) ez = D == 2 ? ngf_z_mma_d2(L, a, B) : ngf_z_mma_d3(L, a, B);
+  if (ez == cudaSuccess) {
+    const dim3 g2((unsigned)((a.pix_hi - a.pix_lo + 255) / 256), (unsigned)K);
+    k_ngf_adj_stream<D><<<g2, 256, 0, L.stream>>>(a, B.Z, B.zlo, B.zstride, B.G, B.vlo, B.vstride);
+    return cudaGetLastError();
+  }
+  if (ez != cudaErrorNotSupported) return ez;
   const int groups = (K + NGF_JG - 1) / NGF_JG;
   const int KP16 = groups * NGF_JG;
   const size_t smem = ((size_t)K * KP16 + (size_t)K * D * NGF_ZP) * 4;

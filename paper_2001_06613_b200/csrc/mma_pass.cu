@@ -132,6 +132,25 @@ static cudaError_t run_pass2_mma(const Launch& L, const Args& a, const float* V,
   return launch_pdl(kern, dim3(grid), dim3(P2M::NT), 0, L.stream, a, V, G, vstride);
 }
 
+template <int D>
+static cudaError_t run_ngf_z_mma(const Launch& L, const Args& a, const NgfBufs& B) {
+  using C = NZ<D>;
+  const int K = a.K;
+  const long long nzp = B.zhi - B.zlo;
+  if (nzp <= 0) return cudaSuccess;
+  if ((long long)K * D * B.zstride >= (1LL << 31)) return cudaErrorNotSupported;
+  const int KS = (K + 7) / 8, JT = (K + 15) / 16;
+  const size_t smem = (size_t)2 * JT * KS * 32 * 16;
+  cudaError_t e = cudaFuncSetAttribute(k_ngf_z_mma<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const long long items = (nzp + C::PW - 1) / C::PW * ((JT + C::MW - 1) / C::MW);
+  const int grid = occupancy_grid(L, k_ngf_z_mma<D>, C::NT, smem, (items + C::NT / 32 - 1) / (C::NT / 32));
+  k_ngf_z_mma<D><<<grid, C::NT, smem, L.stream>>>(a, B.Nf, B.Rho, B.zlo, B.zhi, B.zstride, B.Z);
+  return cudaGetLastError();
+}
+cudaError_t ngf_z_mma_d2(const Launch& L, const Args& a, const NgfBufs& B) { return run_ngf_z_mma<2>(L, a, B); }
+cudaError_t ngf_z_mma_d3(const Launch& L, const Args& a, const NgfBufs& B) { return run_ngf_z_mma<3>(L, a, B); }
+
 cudaError_t sample_gram_d2(const Launch& L, const Args& a, float* V, float* G, long long vstride, double* part,
                            size_t cap, int* nblk) {
   return run_sample_gram<2>(L, a, V, G, vstride, part, cap, nblk);
