@@ -45,11 +45,13 @@ def bytes_per_vf(d: int, s: int) -> dict:
 # reads them back and writes dD/dy; the fused kernels move exactly the SURVEY §8d pass figures
 def kernel_bytes_per_vf(d: int, s: int) -> dict:
     return {"k_sample_v": 2 * (1 + d) * s, "k_gram_tc": s, "k_pass2_stream": (1 + 2 * d) * s,
-            "k_sample_gram": 2 * (1 + d) * s, "k_pass2_mma": (1 + 2 * d) * s,
+            "k_sample_gram": 2 * (1 + d) * s, "k_pass2_mma": (1 + 2 * d) * s, "k_gram_tma": s, "k_gram_mma": s,
+            "k_pass2_bulk": (1 + 2 * d) * s,
             "k_pass2": (1 + 2 * d) * s, "k_pass1_tc": (1 + d) * s, "k_pass1_ws": (1 + d) * s, "k_pass1": (1 + d) * s,
             "k_reduce_finalize": 0,
             # split NGF path: u -> (n, rho); Gram of n; z from (n, rho); adjoint stencil of z with grad T
-            "k_ngf_feat": (2 + d) * s, "k_gram_tcx": d * s, "k_ngf_z": (2 * d + 1) * s, "k_ngf_adj_stream": 3 * d * s}
+            "k_ngf_feat": (2 + d) * s, "k_gram_tcx": d * s, "k_ngf_z": (2 * d + 1) * s, "k_ngf_z_mma": (2 * d + 1) * s,
+            "k_ngf_adj_stream": 3 * d * s}
 
 
 def _peaks():

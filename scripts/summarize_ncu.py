@@ -67,8 +67,27 @@ def main():
     ap.add_argument("--rep", action="append", default=[])
     ap.add_argument("--launches", action="append", default=[])
     ap.add_argument("--out", required=True)
+    ap.add_argument("--traffic-out", help="write {kernel: dram read + write bytes per launch} (bench.py roofline)")
     a = ap.parse_args()
     parts = [launches_summary(p) for p in a.launches] + [rep_summary(p) for p in a.rep]
+    if a.traffic_out:
+        import json
+        tr = {}
+        for p in a.rep:
+            raw = subprocess.run(["ncu", "-i", p, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+            rows = list(csv.reader(io.StringIO(raw)))
+            h, units = rows[0], rows[1]
+            for r in rows[2:]:
+                name = r[h.index("Kernel Name")].replace("void ", "").split("<")[0].split("(")[0].strip()
+                b = 0.0
+                for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                    v = float(r[h.index(m)].replace(",", ""))
+                    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(units[h.index(m)], 1)
+                    b += v * scale
+                tr.setdefault(name, int(b))
+        tr["source"] = "ncu --set full (cold caches): dram__bytes_read.sum + dram__bytes_write.sum per launch, " + ", ".join(a.rep)
+        with open(a.traffic_out, "w") as f:
+            json.dump(tr, f, indent=1)
     with open(a.out, "w") as f:
         f.write("\n".join(parts))
     print(open(a.out).read())
