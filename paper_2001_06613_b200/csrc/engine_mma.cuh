@@ -412,10 +412,11 @@ __device__ __forceinline__ void stsm_x4(uint32_t addr, float c0, float c1, float
 // the six upper m16n8 blocks with 3 HMMAs each (fp32 per <= 8 tiles, fp64 across), per-frame sum /
 // max / min from the A-order fragments (every element lies in exactly one of them).
 struct GTM {
-  static constexpr int KP = 32, TP = 128, NT = 256, NST = 4, BOXP = 32;
-  static constexpr int SBYTES = KP * TP * 4;  // one stage: 4 boxes of [32 rows x 128 B]
+  static constexpr int KP = 32, TP = 128, NT = 256, NST = 3, BOXP = 32;
+  static constexpr int SBYTES = KP * TP * 4;          // one stage: 4 boxes of [32 rows x 128 B]
+  static constexpr int ABYTES = 8 * 6 * 4 * 32 * 8;  // fp64 Gram accumulators [warp][block][r][lane]
 };
-constexpr size_t gtm_smem() { return 1024 + (size_t)GTM::NST * GTM::SBYTES + 256; }
+constexpr size_t gtm_smem() { return 1024 + (size_t)GTM::NST * GTM::SBYTES + 256 + GTM::ABYTES; }
 
 // hi = v with the 13 low mantissa bits cleared (exact in tf32; one LOP3 instead of the ~4-instruction
 // cvt.rna), lo = v - hi exactly (|lo| < 2^-10 |v|, truncated to tf32 by the MMA: 2^-20 relative).
@@ -433,6 +434,8 @@ __global__ void __launch_bounds__(GTM::NT, 2) k_gram_tma(const Args a, const __g
   unsigned char* base = gtm_sh + ((1024 - (smem_u32(gtm_sh) & 1023)) & 1023);
   uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)NST * GTM::SBYTES);
   uint64_t* empty = full + NST;
+  // fp64 accumulators in shared memory (not registers): [warp 8][block 6][r 4][lane 32]
+  double* gsm = reinterpret_cast<double*>(base + (size_t)NST * GTM::SBYTES + 256);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   const int K = a.K;
@@ -474,7 +477,9 @@ __global__ void __launch_bounds__(GTM::NT, 2) k_gram_tma(const Args a, const __g
     }
   const uint32_t sb = smem_u32(base);
   float acc[6][4] = {};
-  double gacc[6][4] = {};
+  double* ga = gsm + warp * 6 * 4 * 32 + lane;  // this lane's accumulators, stride 32
+#pragma unroll
+  for (int e = 0; e < 24; ++e) ga[e * 32] = 0.0;
   float fs[2][2] = {}, fmx[2][2], fmn[2][2];  // [m][h]: rows 16 m + g + 8 h
   double ds[2][2] = {};
 #pragma unroll
@@ -507,22 +512,34 @@ __global__ void __launch_bounds__(GTM::NT, 2) k_gram_tma(const Args a, const __g
     for (int kq = 0; kq < 2; ++kq) {
       // per-frame statistics from the A-order fragments: rows 16 m + g (+ 8), pixels p0 + 8 kq + t (+ 4)
       const long long pc = p0 + 8 * kq + t;
-      const bool ok0 = pc < npix, ok1 = pc + 4 < npix;
+      if (p0 + 16 <= npix) {  // warp-uniform: every pixel of this warp's slice is inside the slab
 #pragma unroll
-      for (int m = 0; m < 2; ++m)
+        for (int m = 0; m < 2; ++m)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const float v0 = __uint_as_float(QA[kq][m][h]), v1 = __uint_as_float(QA[kq][m][2 + h]);
-          fs[m][h] += v0 + v1;  // zero past the slab
-          if (ok0) {
-            fmx[m][h] = fmaxf(fmx[m][h], v0);
-            fmn[m][h] = fminf(fmn[m][h], v0);
+          for (int h = 0; h < 2; ++h) {
+            const float v0 = __uint_as_float(QA[kq][m][h]), v1 = __uint_as_float(QA[kq][m][2 + h]);
+            fs[m][h] += v0 + v1;
+            fmx[m][h] = fmaxf(fmx[m][h], fmaxf(v0, v1));
+            fmn[m][h] = fminf(fmn[m][h], fminf(v0, v1));
           }
-          if (ok1) {
-            fmx[m][h] = fmaxf(fmx[m][h], v1);
-            fmn[m][h] = fminf(fmn[m][h], v1);
+      } else {
+        const bool ok0 = pc < npix, ok1 = pc + 4 < npix;
+#pragma unroll
+        for (int m = 0; m < 2; ++m)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const float v0 = __uint_as_float(QA[kq][m][h]), v1 = __uint_as_float(QA[kq][m][2 + h]);
+            fs[m][h] += v0 + v1;  // zero past the slab
+            if (ok0) {
+              fmx[m][h] = fmaxf(fmx[m][h], v0);
+              fmn[m][h] = fminf(fmn[m][h], v0);
+            }
+            if (ok1) {
+              fmx[m][h] = fmaxf(fmx[m][h], v1);
+              fmn[m][h] = fminf(fmn[m][h], v1);
+            }
           }
-        }
+      }
       uint32_t AH[2][4], AL[2][4], BH[2][4], BL[2][4];
 #pragma unroll
       for (int m = 0; m < 2; ++m) {
@@ -551,7 +568,7 @@ __global__ void __launch_bounds__(GTM::NT, 2) k_gram_tma(const Args a, const __g
       for (int b = 0; b < 6; ++b)
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
-          gacc[b][r] += (double)acc[b][r];
+          ga[(b * 4 + r) * 32] += (double)acc[b][r];
           acc[b][r] = 0.f;
         }
 #pragma unroll
@@ -565,13 +582,9 @@ __global__ void __launch_bounds__(GTM::NT, 2) k_gram_tma(const Args a, const __g
   }
   // ---- CTA reduction (fixed order) through shared memory (the stages are no longer in use)
   __syncthreads();
-  double* red = reinterpret_cast<double*>(base);  // [warp 8][block 6][r 4][lane 32], then stats
-#pragma unroll
-  for (int b = 0; b < 6; ++b)
-#pragma unroll
-    for (int r = 0; r < 4; ++r) red[((warp * 6 + b) * 4 + r) * 32 + lane] = gacc[b][r];
+  const double* red = gsm;  // [warp 8][block 6][r 4][lane 32]
   // per-frame stats: reduce over the 4 lanes t of a row (xor tree), then over warps in smem
-  double* rs = red + 8 * 6 * 4 * 32;  // [warp 8][row 32] x {sum, max, -min}
+  double* rs = reinterpret_cast<double*>(base);  // [warp 8][row 32] x {sum, max, -min} (ring area)
 #pragma unroll
   for (int m = 0; m < 2; ++m)
 #pragma unroll
