@@ -334,7 +334,7 @@ static int pass1_kp(const sr_ctx* c, const sr_problem* p) {
   if (p->dtype == SR_F32 && p->feature == SR_NCC && p->param == SR_DISPLACEMENT && p->k <= 32 && !c->legacy &&
       c->tc)
     return 32;
-  if (ngf_split(c, p)) return p->k <= 64 ? 64 : 128;
+  if (ngf_split(c, p)) return p->k <= 32 && c->mma ? 32 : p->k <= 64 ? 64 : 128;  // 32: TMA-fed mma.sync Gram
   return kp_of(p->k);
 }
 
@@ -380,7 +380,7 @@ static int corr_partial_impl(sr_ctx* c, const sr_problem* p, double* raw, double
   const Launch L = launch_of(c);
   int nblk = 0;
   const long long npix = p->pix_hi - p->pix_lo;
-  if ((KP == 64 || KP == 128) && ngf_split(c, p) && npix > 0) {
+  if ((KP == 32 || KP == 64 || KP == 128) && ngf_split(c, p) && npix > 0) {
     const Geo g = a.g;
     const long long row = g.st[g.nd - 1];
     sr::NgfBufs B{};
@@ -403,8 +403,10 @@ static int corr_partial_impl(sr_ctx* c, const sr_problem* p, double* raw, double
     B.Z = B.Nf + nz * d;
     B.Rho = B.Z + nz * d;
     c->vtag.valid = 0;
-    const cudaError_t e1 = d == 2 ? ngf_pass1_d2(L, a, B, c->part, c->part_cap, &nblk)
-                                  : ngf_pass1_d3(L, a, B, c->part, c->part_cap, &nblk);
+    const cudaError_t e1 = KP == 32 ? (d == 2 ? ngf_pass1_mma_d2(L, a, B, c->part, c->part_cap, &nblk)
+                                              : ngf_pass1_mma_d3(L, a, B, c->part, c->part_cap, &nblk))
+                                    : (d == 2 ? ngf_pass1_d2(L, a, B, c->part, c->part_cap, &nblk)
+                                              : ngf_pass1_d3(L, a, B, c->part, c->part_cap, &nblk));
     if (e1 == cudaSuccess) {
       set_vtag(c, p, B.vstride, 1);
       c->vtag.ngf = B;

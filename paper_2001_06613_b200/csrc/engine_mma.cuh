@@ -428,7 +428,11 @@ __device__ __forceinline__ void split_q(const uint32_t (&q)[4], uint32_t (&h)[4]
   }
 }
 
-__global__ void __launch_bounds__(GTM::NT, 2) k_gram_tma(const Args a, const __grid_constant__ CUtensorMap vmap) {
+// NGF: the same Gram over the feature array n [K][ncomp][zstride] (rows = frames, columns = (component,
+// pixel) tiles of a 3-D map); the statistics slots then carry max |n| (the NGF degeneracy threshold).
+template <bool NGF>
+__global__ void __launch_bounds__(GTM::NT, 2) k_gram_tma(const Args a, const __grid_constant__ CUtensorMap vmap,
+                                                         int ntx) {
   constexpr int KP = GTM::KP, TP = GTM::TP, NST = GTM::NST;
   extern __shared__ __align__(1024) unsigned char gtm_sh[];
   unsigned char* base = gtm_sh + ((1024 - (smem_u32(gtm_sh) & 1023)) & 1023);
@@ -440,7 +444,7 @@ __global__ void __launch_bounds__(GTM::NT, 2) k_gram_tma(const Args a, const __g
   const int g = lane >> 2, t = lane & 3;
   const int K = a.K;
   const long long npix = a.pix_hi - a.pix_lo;
-  const long long ntiles = (npix + TP - 1) / TP;
+  const long long ntiles = (long long)ntx * (NGF ? a.g.nd : 1);  // tile t: component t / ntx, x-tile t % ntx
   const long long nloc = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   if (tid == 0) {
     for (int s2 = 0; s2 < NST; ++s2) {
@@ -454,11 +458,12 @@ __global__ void __launch_bounds__(GTM::NT, 2) k_gram_tma(const Args a, const __g
   pdl_trigger();
   __syncthreads();
   auto issue = [&](long long n, int s2) {
-    const int x0 = (int)((blockIdx.x + n * gridDim.x) * TP);
+    const long long tt = blockIdx.x + n * gridDim.x;
+    const int x0 = (int)(tt % ntx) * TP, c = (int)(tt / ntx);
     unsigned char* st = base + (size_t)s2 * GTM::SBYTES;
     mbar_arrive_expect_tx(&full[s2], (uint32_t)GTM::SBYTES);
 #pragma unroll
-    for (int b = 0; b < TP / GTM::BOXP; ++b) tma_load_2d(st + b * 4096, &vmap, x0 + GTM::BOXP * b, 0, &full[s2]);
+    for (int b = 0; b < TP / GTM::BOXP; ++b) tma_load_3d(st + b * 4096, &vmap, x0 + GTM::BOXP * b, c, 0, &full[s2]);
   };
   if (tid == 0)
     for (long long n = 0; n < nloc && n < NST; ++n) issue(n, (int)n);
@@ -492,7 +497,7 @@ __global__ void __launch_bounds__(GTM::NT, 2) k_gram_tma(const Args a, const __g
   for (long long n = 0; n < nloc; ++n) {
     const int s2 = (int)(n % NST);
     const uint32_t st = sb + (uint32_t)(s2 * GTM::SBYTES);
-    const long long p0 = (blockIdx.x + n * gridDim.x) * TP + 16 * warp;  // this warp's first pixel
+    const long long p0 = ((blockIdx.x + n * gridDim.x) % ntx) * TP + 16 * warp;  // this warp's first pixel
     mbar_wait(&full[s2], (uint32_t)((n / NST) & 1));
     uint32_t QA[2][2][4], QB[2][2][4];
 #pragma unroll
@@ -624,6 +629,13 @@ __global__ void __launch_bounds__(GTM::NT, 2) k_gram_tma(const Args a, const __g
       sv += rs[(w2 * 32 + k) * 3 + 0];
       mx = fmax(mx, rs[(w2 * 32 + k) * 3 + 1]);
       mn = fmin(mn, rs[(w2 * 32 + k) * 3 + 2]);
+    }
+    if (NGF) {  // k_gram_tcx's layout: s unused, both extremum slots = max |n| (0 when no pixel)
+      const double am = k < K && mx >= mn ? fmax(mx, -mn) : 0.0;
+      out[KP * KP + k] = 0.0;
+      out[KP * KP + KP + k] = am;
+      out[KP * KP + 2 * KP + k] = am;
+      return;
     }
     const float* shifts = reinterpret_cast<const float*>(a.shifts);
     const double sh = (k < K && shifts) ? (double)shifts[a.job->frame_index[k]] : 0.0;

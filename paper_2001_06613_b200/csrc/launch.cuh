@@ -350,6 +350,8 @@ cudaError_t run_ngf_pass1(const Launch& L, const Args& a, const NgfBufs& B, doub
 }
 
 cudaError_t ngf_z_mma_d2(const Launch& L, const Args& a, const NgfBufs& B);
+cudaError_t ngf_pass1_mma_d2(const Launch& L, const Args& a, const NgfBufs& B, double* part, size_t cap, int* nblk);
+cudaError_t ngf_pass1_mma_d3(const Launch& L, const Args& a, const NgfBufs& B, double* part, size_t cap, int* nblk);
 cudaError_t ngf_z_mma_d3(const Launch& L, const Args& a, const NgfBufs& B);
 
 template <int D>

@@ -46,6 +46,66 @@ static cudaError_t run_sample_gram(const Launch& L, const Args& a, float* V, flo
   return cudaGetLastError();
 }
 
+// 3-D view [rows][ncomp][npix] (row stride ncomp * stride, component stride `stride` floats) for the
+// TMA-fed Gram: boxes of [32 rows x 1 component x 32 pixels], SWIZZLE_128B, zero fill past the edges
+static bool encode_gram_map(EncodeTiledFn fn, CUtensorMap* m, const float* base, long long npix, int ncomp,
+                            int rows, long long stride) {
+  memset(m, 0, sizeof *m);
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (stride * 4) % 16) return false;
+  cuuint64_t gdim[3] = {(cuuint64_t)npix, (cuuint64_t)ncomp, (cuuint64_t)rows};
+  cuuint64_t gstr[2] = {(cuuint64_t)stride * 4, (cuuint64_t)ncomp * stride * 4};
+  cuuint32_t box[3] = {(cuuint32_t)GTM::BOXP, 1, (cuuint32_t)GTM::KP};
+  cuuint32_t es[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), gdim, gstr, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// split NGF pass 1 for K <= 32: sampling, features, then the TMA-fed mma.sync Gram of n (KP = 32 partials)
+template <int D>
+static cudaError_t run_ngf_pass1_mma(const Launch& L, const Args& a, const NgfBufs& B, double* part,
+                                     size_t part_cap, int* nblk) {
+  const long long npix = a.pix_hi - a.pix_lo;
+  if (npix <= 0 || a.K > GTM::KP) return cudaErrorNotSupported;
+  if (((a.pix_lo - B.zlo) * 4) % 16) return cudaErrorNotSupported;
+  EncodeTiledFn fn = encode_tiled_fn();
+  CUtensorMap xmap;
+  if (!fn || !encode_gram_map(fn, &xmap, B.Nf + (a.pix_lo - B.zlo), npix, D, a.K, B.zstride))
+    return cudaErrorNotSupported;
+  Args av = a;  // u and grad T over [vlo, vhi) (no shift: n only sees differences of u)
+  av.pix_lo = B.vlo;
+  av.pix_hi = B.vhi;
+  av.shifts = nullptr;
+  constexpr int SPT = 4;
+  const dim3 sgrid((unsigned)((B.vhi - B.vlo + 256 * SPT - 1) / (256 * SPT)), (unsigned)a.K);
+  if (a.g.pow2) k_sample_v<D, true, SPT, true><<<sgrid, 256, 0, L.stream>>>(av, B.V, B.G, B.vstride);
+  else k_sample_v<D, false, SPT, true><<<sgrid, 256, 0, L.stream>>>(av, B.V, B.G, B.vstride);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const dim3 fgrid((unsigned)((B.zhi - B.zlo + 255) / 256), (unsigned)a.K);
+  k_ngf_feat<D><<<fgrid, 256, 0, L.stream>>>(a, B.V, B.vlo, B.vstride, B.Nf, B.Rho, B.zlo, B.zhi, B.zstride);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const size_t smem = gtm_smem();
+  e = cudaFuncSetAttribute(k_gram_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int ntx = (int)((npix + GTM::TP - 1) / GTM::TP);
+  int grid = occupancy_grid(L, k_gram_tma<true>, GTM::NT, smem, (long long)ntx * D);
+  const size_t stride = (size_t)GTM::KP * GTM::KP + 3 * GTM::KP;
+  if ((size_t)grid * stride > part_cap) grid = (int)(part_cap / stride);
+  Args b = a;
+  b.part = part;
+  k_gram_tma<true><<<grid, GTM::NT, smem, L.stream>>>(b, xmap, ntx);
+  *nblk = grid;
+  return cudaGetLastError();
+}
+cudaError_t ngf_pass1_mma_d2(const Launch& L, const Args& a, const NgfBufs& B, double* part, size_t cap, int* nblk) {
+  return run_ngf_pass1_mma<2>(L, a, B, part, cap, nblk);
+}
+cudaError_t ngf_pass1_mma_d3(const Launch& L, const Args& a, const NgfBufs& B, double* part, size_t cap, int* nblk) {
+  return run_ngf_pass1_mma<3>(L, a, B, part, cap, nblk);
+}
+
 // split pass 1: k_sample_v (V = v - shift, grad T) then k_gram_mma (Gram + per-frame stats of V)
 template <int D>
 static cudaError_t run_sample_then_gram(const Launch& L, const Args& a, float* V, float* G, long long vstride,
@@ -75,22 +135,15 @@ static cudaError_t run_sample_then_gram(const Launch& L, const Args& a, float* V
   EncodeTiledFn fn = encode_tiled_fn();
   if (fn && !getenv("SEQREG_B200_GRAMREG")) {  // TMA-fed Gram (k_gram_tma)
     CUtensorMap vmap;
-    memset(&vmap, 0, sizeof vmap);
-    cuuint64_t gdim[2] = {(cuuint64_t)npix, (cuuint64_t)a.K};
-    cuuint64_t gstr[1] = {(cuuint64_t)vstride * 4};
-    cuuint32_t box[2] = {(cuuint32_t)GTM::BOXP, (cuuint32_t)GTM::KP};
-    cuuint32_t es[2] = {1, 1};
-    if (fn(&vmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, V, gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
-        CUDA_SUCCESS) {
+    if (encode_gram_map(fn, &vmap, V, npix, 1, a.K, vstride)) {
       const size_t smem = gtm_smem();
-      e = cudaFuncSetAttribute(k_gram_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      e = cudaFuncSetAttribute(k_gram_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
-      int grid = occupancy_grid(L, k_gram_tma, GTM::NT, smem, ntiles);
+      int grid = occupancy_grid(L, k_gram_tma<false>, GTM::NT, smem, ntiles);
       if ((size_t)grid * stride > part_cap) grid = (int)(part_cap / stride);
       Args b = a;
       b.part = part;
-      e = launch_pdl(k_gram_tma, dim3(grid), dim3(GTM::NT), smem, L.stream, b, vmap);
+      e = launch_pdl(k_gram_tma<false>, dim3(grid), dim3(GTM::NT), smem, L.stream, b, vmap, (int)ntiles);
       *nblk = grid;
       return e;
     }
