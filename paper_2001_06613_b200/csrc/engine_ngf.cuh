@@ -48,6 +48,127 @@ __global__ void __launch_bounds__(256) k_ngf_feat(const Args a, const float* __r
   Rho[(long long)k * zstride + (p - zlo)] = rho;
 }
 
+// The same arithmetic as k_ngf_feat (and ngf_at), 4 consecutive pixels per thread: one coordinate
+// decomposition per thread (then incremented), 32-bit offsets inside a frame's plane, 128-bit stores of
+// n and rho when the z plane allows them.  (k_ngf_feat: ~200 instructions per pixel, issue-bound.)
+template <int D>
+__global__ void __launch_bounds__(256) k_ngf_feat4(const Args a, const float* __restrict__ V, long long vlo,
+                                                   long long vstride, float* __restrict__ Nf, float* __restrict__ Rho,
+                                                   long long zlo, long long zhi, long long zstride) {
+  const int k = blockIdx.y;
+  const int nz = (int)(zhi - zlo);
+  const int q0 = (blockIdx.x * 256 + threadIdx.x) * 4;  // z-relative first pixel
+  if (q0 >= nz) return;
+  const float* u = V + (long long)k * vstride + (zlo - vlo);  // u[q]: pixel zlo + q
+  float* nb = Nf + (long long)k * D * zstride;
+  float* rb = Rho + (long long)k * zstride;
+  const int p0 = (int)zlo + q0;
+  int c[3];
+  coords_flat(a.g, p0, c);
+  const float e = (float)a.eps;
+  float nv[D][4], rv[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int q = q0 + t;
+    float g[D], pn = 0.f;
+#pragma unroll
+    for (int ax = 0; ax < D; ++ax) {
+      const bool hp = c[ax] < a.g.n[ax] - 1, hm = c[ax] > 0;
+      const int st = a.g.sti[ax];
+      const float up = __ldg(u + (hp ? q + st : q)), um = __ldg(u + (hm ? q - st : q));
+      const float inv = a.g.invf[ax];
+      g[ax] = (hp && hm) ? (up - um) * (inv * 0.5f) : (up - um) * inv;
+      pn += g[ax] * g[ax];
+    }
+    const float rho = sqrtf(pn + e * e);
+    const float ir = 1.f / rho;
+#pragma unroll
+    for (int ax = 0; ax < D; ++ax) nv[ax][t] = g[ax] * ir;
+    rv[t] = rho;
+    if (++c[0] == a.g.n[0]) {  // next pixel
+      c[0] = 0;
+      if (D > 1 && ++c[1] == a.g.n[1]) {
+        c[1] = 0;
+        ++c[2];
+      }
+    }
+  }
+  if (q0 + 4 <= nz && (zstride & 3) == 0) {
+#pragma unroll
+    for (int ax = 0; ax < D; ++ax)
+      *reinterpret_cast<float4*>(nb + ax * zstride + q0) = make_float4(nv[ax][0], nv[ax][1], nv[ax][2], nv[ax][3]);
+    *reinterpret_cast<float4*>(rb + q0) = make_float4(rv[0], rv[1], rv[2], rv[3]);
+  } else {
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (q0 + t < nz) {
+#pragma unroll
+        for (int ax = 0; ax < D; ++ax) nb[ax * zstride + q0 + t] = nv[ax][t];
+        rb[q0 + t] = rv[t];
+      }
+  }
+}
+
+// k_ngf_adj_stream with 4 consecutive pixels per thread (same arithmetic as dgrad_adjoint), 128-bit
+// grad T loads and dD/dy stores when aligned.
+template <int D>
+__global__ void __launch_bounds__(256) k_ngf_adj4(const Args a, const float* __restrict__ Z, long long zlo,
+                                                  long long zstride, const float* __restrict__ Gv, long long vlo,
+                                                  long long vstride) {
+  const int k = blockIdx.y;
+  const int npix = (int)(a.pix_hi - a.pix_lo);
+  const int q0 = (blockIdx.x * 256 + threadIdx.x) * 4;  // slab-relative first pixel
+  if (q0 >= npix) return;
+  const int p0 = (int)a.pix_lo + q0;
+  int c[3];
+  coords_flat(a.g, p0, c);
+  float du[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    float acc = 0.f;
+#pragma unroll
+    for (int ax = 0; ax < D; ++ax) {
+      const float* z = Z + ((long long)k * D + ax) * zstride + (p0 - zlo);
+      const int st = a.g.sti[ax], i = c[ax], n = a.g.n[ax];
+      const float inv = a.g.invf[ax];
+      const float h2 = inv * 0.5f;
+      float o = 0.f;  // dgrad_adjoint: rows i - 1, i + 1 (interior) and the one-sided edge rows
+      if (i - 1 >= 1 && i - 1 <= n - 2) o += __ldg(z + t - st) * h2;
+      if (i + 1 >= 1 && i + 1 <= n - 2) o -= __ldg(z + t + st) * h2;
+      if (i == 0) o -= __ldg(z + t) * inv;
+      if (i == 1) o += __ldg(z + t - st) * inv;
+      if (i == n - 1) o += __ldg(z + t) * inv;
+      if (i == n - 2) o -= __ldg(z + t + st) * inv;
+      acc += o;
+    }
+    du[t] = acc;
+    if (++c[0] == a.g.n[0]) {
+      c[0] = 0;
+      if (D > 1 && ++c[1] == a.g.n[1]) {
+        c[1] = 0;
+        ++c[2];
+      }
+    }
+  }
+  float* out = reinterpret_cast<float*>(a.out);
+  const long long go = (long long)(p0 - vlo), oo = (long long)p0 - a.o_off;
+  const bool vec = q0 + 4 <= npix && ((go | vstride) & 3) == 0 && ((oo | a.o_stride) & 3) == 0 &&
+                   ((reinterpret_cast<uintptr_t>(Gv) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+#pragma unroll
+  for (int cc = 0; cc < D; ++cc) {
+    const float* gs = Gv + ((long long)k * D + cc) * vstride + go;
+    float* dst = out + ((long long)k * D + cc) * a.o_stride + oo;
+    if (vec) {
+      const float4 gv = __ldg(reinterpret_cast<const float4*>(gs));
+      *reinterpret_cast<float4*>(dst) = make_float4(du[0] * gv.x, du[1] * gv.y, du[2] * gv.z, du[3] * gv.w);
+    } else {
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (q0 + t < npix) dst[t] = du[t] * __ldg(gs + t);
+    }
+  }
+}
+
 // ------------------------------------------------------------------------------------------
 // Raw NGF Gram G_ij = sum over the slab's pixels and components of n_i n_j, for up to 128 frames.
 // Tiles of 32 columns of one component ([128 frames x 32] TMA box of a 3-D map over

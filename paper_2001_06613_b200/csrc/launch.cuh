@@ -323,8 +323,8 @@ cudaError_t run_ngf_pass1_kp(const Launch& L, const Args& a, const NgfBufs& B, d
   else k_sample_v<D, false, SPT, true><<<sgrid, 256, 0, L.stream>>>(av, B.V, B.G, B.vstride);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const dim3 fgrid((unsigned)((B.zhi - B.zlo + 255) / 256), (unsigned)a.K);
-  k_ngf_feat<D><<<fgrid, 256, 0, L.stream>>>(a, B.V, B.vlo, B.vstride, B.Nf, B.Rho, B.zlo, B.zhi, B.zstride);
+  const dim3 fgrid((unsigned)((B.zhi - B.zlo + 1023) / 1024), (unsigned)a.K);
+  k_ngf_feat4<D><<<fgrid, 256, 0, L.stream>>>(a, B.V, B.vlo, B.vstride, B.Nf, B.Rho, B.zlo, B.zhi, B.zstride);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const size_t smem = tgx_smem<KP>();
@@ -361,8 +361,8 @@ cudaError_t run_ngf_pass2(const Launch& L, const Args& a, const NgfBufs& B) {
   cudaError_t ez = cudaErrorNotSupported;
   if (zmma) ez = D == 2 ? ngf_z_mma_d2(L, a, B) : ngf_z_mma_d3(L, a, B);
   if (ez == cudaSuccess) {
-    const dim3 g2((unsigned)((a.pix_hi - a.pix_lo + 255) / 256), (unsigned)K);
-    k_ngf_adj_stream<D><<<g2, 256, 0, L.stream>>>(a, B.Z, B.zlo, B.zstride, B.G, B.vlo, B.vstride);
+    const dim3 g2((unsigned)((a.pix_hi - a.pix_lo + 1023) / 1024), (unsigned)K);
+    k_ngf_adj4<D><<<g2, 256, 0, L.stream>>>(a, B.Z, B.zlo, B.zstride, B.G, B.vlo, B.vstride);
     return cudaGetLastError();
   }
   if (ez != cudaErrorNotSupported) return ez;
@@ -375,8 +375,8 @@ cudaError_t run_ngf_pass2(const Launch& L, const Args& a, const NgfBufs& B) {
       a, B.Nf, B.Rho, B.zlo, B.zhi, B.zstride, B.Z);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const dim3 g2((unsigned)((a.pix_hi - a.pix_lo + 255) / 256), (unsigned)K);
-  k_ngf_adj_stream<D><<<g2, 256, 0, L.stream>>>(a, B.Z, B.zlo, B.zstride, B.G, B.vlo, B.vstride);
+  const dim3 g2((unsigned)((a.pix_hi - a.pix_lo + 1023) / 1024), (unsigned)K);
+  k_ngf_adj4<D><<<g2, 256, 0, L.stream>>>(a, B.Z, B.zlo, B.zstride, B.G, B.vlo, B.vstride);
   return cudaGetLastError();
 }
 cudaError_t ngf_pass1_d2(const Launch& L, const Args& a, const NgfBufs& B, double* part, size_t cap, int* nblk);

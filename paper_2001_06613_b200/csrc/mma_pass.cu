@@ -82,8 +82,8 @@ static cudaError_t run_ngf_pass1_mma(const Launch& L, const Args& a, const NgfBu
   else k_sample_v<D, false, SPT, true><<<sgrid, 256, 0, L.stream>>>(av, B.V, B.G, B.vstride);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const dim3 fgrid((unsigned)((B.zhi - B.zlo + 255) / 256), (unsigned)a.K);
-  k_ngf_feat<D><<<fgrid, 256, 0, L.stream>>>(a, B.V, B.vlo, B.vstride, B.Nf, B.Rho, B.zlo, B.zhi, B.zstride);
+  const dim3 fgrid((unsigned)((B.zhi - B.zlo + 1023) / 1024), (unsigned)a.K);
+  k_ngf_feat4<D><<<fgrid, 256, 0, L.stream>>>(a, B.V, B.vlo, B.vstride, B.Nf, B.Rho, B.zlo, B.zhi, B.zstride);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const size_t smem = gtm_smem();
