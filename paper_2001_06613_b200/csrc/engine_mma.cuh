@@ -16,6 +16,8 @@
 // The legacy tensor path runs ~270 TFLOP/s tf32 on B200 (scripts/probe_mma_sync.cu); each pass
 // needs ~1.6 GFLOP at C2, on a pipe the sampling and streaming instructions do not use.
 #pragma once
+#include <cuda_fp16.h>
+
 #include "engine.cuh"
 #include "tma.cuh"
 
@@ -1085,6 +1087,182 @@ __global__ void __launch_bounds__(NZ<D>::NT, 1) k_ngf_z_mma(const Args a, const 
             r[c][1] = acc[m][2 * c][2 * h + 1];
             r[c][2] = acc[m][2 * c + 1][2 * h];
             r[c][3] = acc[m][2 * c + 1][2 * h + 1];
+          }
+          if (fullb) {
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+              const float4 v = __ldg(reinterpret_cast<const float4*>(Nf + ((j * D + c) * zs + pz)));
+              n[c][0] = v.x, n[c][1] = v.y, n[c][2] = v.z, n[c][3] = v.w;
+            }
+            const float4 v = __ldg(reinterpret_cast<const float4*>(Rho + (j * zs + pz)));
+            rho[0] = v.x, rho[1] = v.y, rho[2] = v.z, rho[3] = v.w;
+          } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const bool ok = pz + u < nzp;
+#pragma unroll
+              for (int c = 0; c < D; ++c) n[c][u] = ok ? Nf[(j * D + c) * zs + pz + u] : 0.f;
+              rho[u] = ok ? Rho[j * zs + pz + u] : 1.f;
+            }
+          }
+          float zz[D][4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            float dot = 0.f;
+#pragma unroll
+            for (int c = 0; c < D; ++c) dot += n[c][u] * r[c][u];
+            const float ir = 1.f / rho[u];
+#pragma unroll
+            for (int c = 0; c < D; ++c) zz[c][u] = (r[c][u] - n[c][u] * dot) * ir;
+          }
+#pragma unroll
+          for (int c = 0; c < D; ++c) {
+            float* dst = Z + ((j * D + c) * zs + pz);
+            if (fullb) {
+              *reinterpret_cast<float4*>(dst) = make_float4(zz[c][0], zz[c][1], zz[c][2], zz[c][3]);
+            } else {
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (pz + u < nzp) dst[u] = zz[c][u];
+            }
+          }
+        }
+      }
+  }
+}
+
+__device__ __forceinline__ void mma_f16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// (x0, x1) -> packed f16 hi and lo halves: hi = f16(x), lo = f16(x - hi) (x ~ hi + lo to 2^-22 relative)
+__device__ __forceinline__ void split_h2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(x0, x1);
+  const float2 hf = __half22float2(h);
+  const __half2 l = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+
+// k_ngf_z_mma with f16 operands (default): the legacy tensor path runs m16n8k16 f16 at twice the
+// tf32 rate (scripts/probe_mma_sync.cu), so each product takes 3 f16 HMMAs per 16 frames instead of per 8.
+// 2-way split: x = hi + lo, hi = f16(x), lo = f16(x - hi): 22 significant bits, products exact in the
+// fp32 accumulator, a.b ~ hi hi + lo hi + hi lo.  n is in [-1, 1] (normalised gradients); M' is scaled by
+// 2^s (max |M'| 2^s in [2^13, 2^14), exact) so that it sits in the f16 normal range, and r = acc 2^-s.
+template <int D>
+__global__ void __launch_bounds__(NZ<D>::NT, 1) k_ngf_z_f16(const Args a, const float* __restrict__ Nf,
+                                                           const float* __restrict__ Rho, long long zlo,
+                                                           long long zhi, long long zstride, float* __restrict__ Z) {
+  using C = NZ<D>;
+  constexpr int MW = C::MW, NTL = C::NTL, PW = C::PW;
+  extern __shared__ __align__(16) uint4 nzh_sh[];
+  __shared__ float red_max[32];
+  const int K = a.K;
+  const int KS = (K + 15) / 16, JT = (K + 15) / 16;  // k-steps of 16 frames, m-tiles
+  uint4* Ah = nzh_sh;                 // [JT][KS][32] packed hi {a0..a3}
+  uint4* Al = nzh_sh + JT * KS * 32;  // lo
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const StatsLayout L(K);
+  const double* Md = a.stats + L.M;
+  // scale: 2^s with max |M'| 2^s in [2^13, 2^14)
+  float mx = 0.f;
+  for (int e = tid; e < K * K; e += C::NT) mx = fmaxf(mx, fabsf((float)Md[e]));
+  mx = warp_max(mx);
+  if (lane == 0) red_max[warp] = mx;
+  __syncthreads();
+  if (warp == 0) {
+    float v = lane < C::NT / 32 ? red_max[lane] : 0.f;
+    v = warp_max(v);
+    if (lane == 0) red_max[0] = v;
+  }
+  __syncthreads();
+  const float mmax = red_max[0];
+  const int sexp = mmax > 0.f ? 13 - ilogbf(mmax) : 0;
+  const float scale = ldexpf(1.f, sexp), unscale = ldexpf(1.f, -sexp);
+  for (int e = tid; e < JT * KS * 32; e += C::NT) {
+    const int m = e / (KS * 32), ks = (e / 32) % KS, ln = e & 31;
+    const int gg = ln >> 2, tt = ln & 3;
+    uint32_t hv[4], lv[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {  // a_r = (row g + 8 (r & 1), frames 16 ks + 2t + 8 (r >> 1) + {0, 1}); A[j][i] = M'[i][j]
+      const int j = 16 * m + gg + 8 * (r & 1), i = 16 * ks + 2 * tt + 8 * (r >> 1);
+      const float m0 = (i < K && j < K) ? (float)Md[i * K + j] * scale : 0.f;
+      const float m1 = (i + 1 < K && j < K) ? (float)Md[(i + 1) * K + j] * scale : 0.f;
+      split_h2(m0, m1, hv[r], lv[r]);
+    }
+    Ah[e] = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+    Al[e] = make_uint4(lv[0], lv[1], lv[2], lv[3]);
+  }
+  __syncthreads();
+  const int nzp = (int)(zhi - zlo);
+  const int zs = (int)zstride;
+  const int nblk = (nzp + PW - 1) / PW;
+  const int ngrp = (JT + MW - 1) / MW;
+  const bool vec = (zs & 3) == 0 && ((reinterpret_cast<uintptr_t>(Nf) | reinterpret_cast<uintptr_t>(Rho) |
+                                     reinterpret_cast<uintptr_t>(Z)) & 15) == 0;
+  for (int item = blockIdx.x * (C::NT / 32) + warp; item < nblk * ngrp; item += gridDim.x * (C::NT / 32)) {
+    const int blk = item / ngrp, m0 = (item % ngrp) * MW;
+    const int mc = min(MW, JT - m0);
+    const int p0 = blk * PW;
+    const bool fullb = p0 + PW <= nzp && vec;
+    float acc[MW][NTL][4];
+#pragma unroll
+    for (int m = 0; m < MW; ++m)
+#pragma unroll
+      for (int nt = 0; nt < NTL; ++nt)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[m][nt][r] = 0.f;
+    int pq[2];
+    bool okq[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      pq[q] = p0 + 4 * (g >> 1) + 2 * q + (g & 1);
+      okq[q] = pq[q] < nzp;
+    }
+    for (int ks = 0; ks < KS; ++ks) {
+      uint32_t bh[NTL][2], bl[NTL][2];
+#pragma unroll
+      for (int nt = 0; nt < NTL; ++nt)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {  // b_u = (frames 16 ks + 2t + 8u + {0, 1}, column g)
+          const int i = 16 * ks + 2 * t + 8 * u, c = nt >> 1, q = nt & 1;
+          const float v0 = (i < K && okq[q]) ? __ldg(Nf + ((i * D + c) * zs + pq[q])) : 0.f;
+          const float v1 = (i + 1 < K && okq[q]) ? __ldg(Nf + (((i + 1) * D + c) * zs + pq[q])) : 0.f;
+          split_h2(v0, v1, bh[nt][u], bl[nt][u]);
+        }
+#pragma unroll
+      for (int m = 0; m < MW; ++m) {
+        if (m < mc) {
+          const uint4 ah = Ah[((m0 + m) * KS + ks) * 32 + lane], al = Al[((m0 + m) * KS + ks) * 32 + lane];
+          const uint32_t AH[4] = {ah.x, ah.y, ah.z, ah.w}, AL[4] = {al.x, al.y, al.z, al.w};
+#pragma unroll
+          for (int nt = 0; nt < NTL; ++nt) {
+            mma_f16(acc[m][nt], AH, bh[nt][0], bh[nt][1]);
+            mma_f16(acc[m][nt], AL, bh[nt][0], bh[nt][1]);
+            mma_f16(acc[m][nt], AH, bl[nt][0], bl[nt][1]);
+          }
+        }
+      }
+    }
+    const int pz = p0 + 4 * t;
+#pragma unroll
+    for (int m = 0; m < MW; ++m)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = 16 * (m0 + m) + g + 8 * h;
+        if (m < mc && j < K) {
+          float r[D][4], n[D][4], rho[4];
+#pragma unroll
+          for (int c = 0; c < D; ++c) {
+            r[c][0] = acc[m][2 * c][2 * h] * unscale;
+            r[c][1] = acc[m][2 * c][2 * h + 1] * unscale;
+            r[c][2] = acc[m][2 * c + 1][2 * h] * unscale;
+            r[c][3] = acc[m][2 * c + 1][2 * h + 1] * unscale;
           }
           if (fullb) {
 #pragma unroll

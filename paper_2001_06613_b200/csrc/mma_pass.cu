@@ -192,11 +192,23 @@ static cudaError_t run_ngf_z_mma(const Launch& L, const Args& a, const NgfBufs& 
   const long long nzp = B.zhi - B.zlo;
   if (nzp <= 0) return cudaSuccess;
   if ((long long)K * D * B.zstride >= (1LL << 31)) return cudaErrorNotSupported;
-  const int KS = (K + 7) / 8, JT = (K + 15) / 16;
+  const int JT = (K + 15) / 16;
+  const long long items = (nzp + C::PW - 1) / C::PW * ((JT + C::MW - 1) / C::MW);
+  // SEQREG_B200_NGFZ=2: tf32 operands (k_ngf_z_mma); default f16 operands (k_ngf_z_f16)
+  static const bool tf32 = getenv("SEQREG_B200_NGFZ") && getenv("SEQREG_B200_NGFZ")[0] == '2';
+  if (!tf32) {
+    const int KS = (K + 15) / 16;
+    const size_t smem = (size_t)2 * JT * KS * 32 * 16;
+    cudaError_t e = cudaFuncSetAttribute(k_ngf_z_f16<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int grid = occupancy_grid(L, k_ngf_z_f16<D>, C::NT, smem, (items + C::NT / 32 - 1) / (C::NT / 32));
+    k_ngf_z_f16<D><<<grid, C::NT, smem, L.stream>>>(a, B.Nf, B.Rho, B.zlo, B.zhi, B.zstride, B.Z);
+    return cudaGetLastError();
+  }
+  const int KS = (K + 7) / 8;
   const size_t smem = (size_t)2 * JT * KS * 32 * 16;
   cudaError_t e = cudaFuncSetAttribute(k_ngf_z_mma<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const long long items = (nzp + C::PW - 1) / C::PW * ((JT + C::MW - 1) / C::MW);
   const int grid = occupancy_grid(L, k_ngf_z_mma<D>, C::NT, smem, (items + C::NT / 32 - 1) / (C::NT / 32));
   k_ngf_z_mma<D><<<grid, C::NT, smem, L.stream>>>(a, B.Nf, B.Rho, B.zlo, B.zhi, B.zstride, B.Z);
   return cudaGetLastError();

@@ -7,6 +7,7 @@ oracle's D and dD/dy: each variant runs the fp32 field parity cases in a fresh p
     SEQREG_B200_P2S=0     re-gathering pass 2 (default: streaming pass 2 from the split pass 1's V, grad T)
     SEQREG_B200_SPLIT=0   fused tcgen05 pass 1 (default: sampling kernel + tcgen05 Gram kernel)
     SEQREG_B200_GRAPH=0   no CUDA-graph replay of repeated sr_evaluate calls
+    SEQREG_B200_NGFZ=2    NGF z contraction with tf32 operands (default f16); =0: the SIMT k_ngf_z
     SEQREG_B200_MMA=0     k_sample_v + k_gram_tc + k_pass2_stream (default: k_sample_gram + k_pass2_mma)
     SEQREG_B200_WS2=1     warp-specialized SIMT pass 2
 """
@@ -30,7 +31,9 @@ from oracle import seqreg_oracle as orc
 from scipy.ndimage import gaussian_filter
 
 out = []
-for dims, K, seed in [((64, 48), 32, 1), ((40, 36), 20, 2), ((200, 150), 32, 3), ((12, 11, 10), 32, 4)]:
+for feature, dims, K, seed in [("ncc", (64, 48), 32, 1), ("ncc", (40, 36), 20, 2), ("ncc", (200, 150), 32, 3),
+                               ("ncc", (12, 11, 10), 32, 4), ("ngf", (64, 48), 32, 5), ("ngf", (40, 36), 60, 6),
+                               ("ngf", (12, 11, 10), 20, 7)]:
     rng = np.random.default_rng(seed)
     d = len(dims)
     sp = tuple([0.5, 0.25, 0.75][:d])
@@ -49,22 +52,22 @@ for dims, K, seed in [((64, 48), 32, 1), ((40, 36), 20, 2), ((200, 150), 32, 3),
     w = rng.uniform(0.5, 1.0, K)
     h = float(np.prod(sp))
     fd = srb.DeviceFrames.from_array(srb.get_engine(), frames, srb.GridSpec(dims, sp, org), torch.float32)
-    obj = srb.FieldObjective(fd, list(range(K)), w, h)
+    obj = srb.FieldObjective(fd, list(range(K)), w, h, feature=feature, ngf_eps=0.2)
     yt = torch.as_tensor(y).to(device=fd.data.device, dtype=torch.float32).contiguous()
     stats, g = obj.evaluate(yt)
     D = float(stats[0].item())
     q = frames.astype(np.float32).astype(np.float64)
     yq = y.astype(np.float32).astype(np.float64)
-    _, Dref, gref = orc.evaluate_field(list(q), dims, sp, org, yq, w, h)
+    _, Dref, gref = orc.evaluate_field(list(q), dims, sp, org, yq, w, h, feature, 0.2)
     gd = g.double().cpu().numpy()
-    out.append({"dims": list(dims), "K": K, "dD": abs(D - Dref) / abs(Dref),
+    out.append({"feature": feature, "dims": list(dims), "K": K, "dD": abs(D - Dref) / abs(Dref),
                 "dg": float(np.abs(gd - gref).max() / np.abs(gref).max())})
 print(json.dumps(out))
 """
 
 
 @pytest.mark.parametrize("env", ["SEQREG_B200_LEGACY=1", "SEQREG_B200_TC=0", "SEQREG_B200_TC2=1", "SEQREG_B200_P2S=0",
-                                 "SEQREG_B200_SPLIT=0", "SEQREG_B200_WS2=1", "SEQREG_B200_MMA=0", "SEQREG_B200_GRAPH=0", ""])
+                                 "SEQREG_B200_SPLIT=0", "SEQREG_B200_WS2=1", "SEQREG_B200_MMA=0", "SEQREG_B200_GRAPH=0", "SEQREG_B200_NGFZ=2", "SEQREG_B200_NGFZ=0", ""])
 def test_variant_parity(env):
     e = dict(os.environ)
     if env:
