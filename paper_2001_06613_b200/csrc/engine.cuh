@@ -803,11 +803,17 @@ __global__ void __launch_bounds__(1024) k_reduce_finalize(const double* __restri
   const bool is_max = e >= KP * KP + KP && e < stride;
   double acc = is_max ? -INFINITY : 0.0;
   if (e < stride) {
-    int b = warp;
-#pragma unroll 4
-    for (; b < nblk; b += 32) {
-      const double v = __ldcg(part + (size_t)b * stride + e);
-      acc = is_max ? fmax(acc, v) : acc + v;
+    // all of this lane's partials in flight at once (up to 16 per warp, i.e. 512 CTAs), then the
+    // fixed-order sum; beyond that, batches of 16
+    for (int b0 = warp; b0 < nblk; b0 += 32 * 16) {
+      double v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int b = b0 + 32 * u;
+        v[u] = b < nblk ? __ldcg(part + (size_t)b * stride + e) : (is_max ? -INFINITY : 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) acc = is_max ? fmax(acc, v[u]) : acc + v[u];
     }
   }
   buf[warp][lane] = acc;

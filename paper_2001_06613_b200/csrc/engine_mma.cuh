@@ -760,20 +760,22 @@ __global__ void __launch_bounds__(P2M::NT, MINB) k_pass2_mma(const Args a, const
           bh[nt][u] = __float_as_uint(bv[ks][nt][u]) & 0xffffe000u;
           bl[nt][u] = __float_as_uint(bv[ks][nt][u] - __uint_as_float(bh[nt][u]));
         }
+      uint32_t AH[2][4], AL[2][4];
 #pragma unroll
       for (int m = 0; m < 2; ++m) {
         const float4 ah = Ah[(m * 4 + ks) * 32 + lane], al = Al[(m * 4 + ks) * 32 + lane];
-        const uint32_t AH[4] = {__float_as_uint(ah.x), __float_as_uint(ah.y), __float_as_uint(ah.z),
-                                __float_as_uint(ah.w)};
-        const uint32_t AL[4] = {__float_as_uint(al.x), __float_as_uint(al.y), __float_as_uint(al.z),
-                                __float_as_uint(al.w)};
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-          mma_tf32(acc[m][nt], AH, bh[nt][0], bh[nt][1]);
-          mma_tf32(acc[m][nt], AL, bh[nt][0], bh[nt][1]);
-          mma_tf32(acc[m][nt], AH, bl[nt][0], bl[nt][1]);
-        }
+        AH[m][0] = __float_as_uint(ah.x), AH[m][1] = __float_as_uint(ah.y);
+        AH[m][2] = __float_as_uint(ah.z), AH[m][3] = __float_as_uint(ah.w);
+        AL[m][0] = __float_as_uint(al.x), AL[m][1] = __float_as_uint(al.y);
+        AL[m][2] = __float_as_uint(al.z), AL[m][3] = __float_as_uint(al.w);
       }
+      // one product at a time over the four (m, n-tile) accumulators: consecutive HMMAs are independent
+#pragma unroll
+      for (int mn = 0; mn < 4; ++mn) mma_tf32(acc[mn >> 1][mn & 1], AH[mn >> 1], bh[mn & 1][0], bh[mn & 1][1]);
+#pragma unroll
+      for (int mn = 0; mn < 4; ++mn) mma_tf32(acc[mn >> 1][mn & 1], AL[mn >> 1], bh[mn & 1][0], bh[mn & 1][1]);
+#pragma unroll
+      for (int mn = 0; mn < 4; ++mn) mma_tf32(acc[mn >> 1][mn & 1], AH[mn >> 1], bl[mn & 1][0], bl[mn & 1][1]);
     }
     // epilogue: acc[m][nt][2h + u] = q_j(p0 + 4t + 2 nt + u), j = 16 m + g + 8 h; one 128-bit store per (j, c)
 #pragma unroll
@@ -928,12 +930,13 @@ __global__ void __launch_bounds__(P2B<D>::NT, 1) k_pass2_bulk(const Args a, cons
                                 __float_as_uint(ah.w)};
         const uint32_t AL[4] = {__float_as_uint(al.x), __float_as_uint(al.y), __float_as_uint(al.z),
                                 __float_as_uint(al.w)};
+        // one product at a time over the n-tiles: consecutive HMMAs hit independent accumulators
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt) {
-          mma_tf32(acc[m][nt], AH, bh[nt][0], bh[nt][1]);
-          mma_tf32(acc[m][nt], AL, bh[nt][0], bh[nt][1]);
-          mma_tf32(acc[m][nt], AH, bl[nt][0], bl[nt][1]);
-        }
+        for (int nt = 0; nt < 4; ++nt) mma_tf32(acc[m][nt], AH, bh[nt][0], bh[nt][1]);
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) mma_tf32(acc[m][nt], AL, bh[nt][0], bh[nt][1]);
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) mma_tf32(acc[m][nt], AH, bl[nt][0], bl[nt][1]);
       }
     }
     __syncwarp();  // every lane's V reads are done before Q overwrites the tile
@@ -1063,12 +1066,13 @@ __global__ void __launch_bounds__(NZ<D>::NT, 1) k_ngf_z_mma(const Args a, const 
                                   __float_as_uint(ah.w)};
           const uint32_t AL[4] = {__float_as_uint(al.x), __float_as_uint(al.y), __float_as_uint(al.z),
                                   __float_as_uint(al.w)};
+          // one product at a time over the n-tiles: consecutive HMMAs hit independent accumulators
 #pragma unroll
-          for (int nt = 0; nt < NTL; ++nt) {
-            mma_tf32(acc[m][nt], AH, bh[nt][0], bh[nt][1]);
-            mma_tf32(acc[m][nt], AL, bh[nt][0], bh[nt][1]);
-            mma_tf32(acc[m][nt], AH, bl[nt][0], bl[nt][1]);
-          }
+          for (int nt = 0; nt < NTL; ++nt) mma_tf32(acc[m][nt], AH, bh[nt][0], bh[nt][1]);
+#pragma unroll
+          for (int nt = 0; nt < NTL; ++nt) mma_tf32(acc[m][nt], AL, bh[nt][0], bh[nt][1]);
+#pragma unroll
+          for (int nt = 0; nt < NTL; ++nt) mma_tf32(acc[m][nt], AH, bl[nt][0], bl[nt][1]);
         }
       }
     }
@@ -1224,28 +1228,39 @@ __global__ void __launch_bounds__(NZ<D>::NT, 1) k_ngf_z_f16(const Args a, const 
       pq[q] = p0 + 4 * (g >> 1) + 2 * q + (g & 1);
       okq[q] = pq[q] < nzp;
     }
+    // n values of k-step ks: b_u = (frames 16 ks + 2t + 8u + {0, 1}, column g); the next k-step's are
+    // loaded before this one's MMAs (one step of software pipelining: no exposed load latency per k-step)
+    auto load_n = [&](int ks, float (&nv)[NTL][2][2]) {
+#pragma unroll
+      for (int nt = 0; nt < NTL; ++nt)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int i = 16 * ks + 2 * t + 8 * u, c = nt >> 1, q = nt & 1;
+          nv[nt][u][0] = (i < K && okq[q]) ? __ldg(Nf + ((i * D + c) * zs + pq[q])) : 0.f;
+          nv[nt][u][1] = (i + 1 < K && okq[q]) ? __ldg(Nf + (((i + 1) * D + c) * zs + pq[q])) : 0.f;
+        }
+    };
+    float nvc[NTL][2][2];
+    load_n(0, nvc);
     for (int ks = 0; ks < KS; ++ks) {
       uint32_t bh[NTL][2], bl[NTL][2];
 #pragma unroll
       for (int nt = 0; nt < NTL; ++nt)
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {  // b_u = (frames 16 ks + 2t + 8u + {0, 1}, column g)
-          const int i = 16 * ks + 2 * t + 8 * u, c = nt >> 1, q = nt & 1;
-          const float v0 = (i < K && okq[q]) ? __ldg(Nf + ((i * D + c) * zs + pq[q])) : 0.f;
-          const float v1 = (i + 1 < K && okq[q]) ? __ldg(Nf + (((i + 1) * D + c) * zs + pq[q])) : 0.f;
-          split_h2(v0, v1, bh[nt][u], bl[nt][u]);
-        }
+        for (int u = 0; u < 2; ++u) split_h2(nvc[nt][u][0], nvc[nt][u][1], bh[nt][u], bl[nt][u]);
+      if (ks + 1 < KS) load_n(ks + 1, nvc);
 #pragma unroll
       for (int m = 0; m < MW; ++m) {
         if (m < mc) {
           const uint4 ah = Ah[((m0 + m) * KS + ks) * 32 + lane], al = Al[((m0 + m) * KS + ks) * 32 + lane];
           const uint32_t AH[4] = {ah.x, ah.y, ah.z, ah.w}, AL[4] = {al.x, al.y, al.z, al.w};
+          // one product at a time over the n-tiles: consecutive HMMAs hit independent accumulators
 #pragma unroll
-          for (int nt = 0; nt < NTL; ++nt) {
-            mma_f16(acc[m][nt], AH, bh[nt][0], bh[nt][1]);
-            mma_f16(acc[m][nt], AL, bh[nt][0], bh[nt][1]);
-            mma_f16(acc[m][nt], AH, bl[nt][0], bl[nt][1]);
-          }
+          for (int nt = 0; nt < NTL; ++nt) mma_f16(acc[m][nt], AH, bh[nt][0], bh[nt][1]);
+#pragma unroll
+          for (int nt = 0; nt < NTL; ++nt) mma_f16(acc[m][nt], AL, bh[nt][0], bh[nt][1]);
+#pragma unroll
+          for (int nt = 0; nt < NTL; ++nt) mma_f16(acc[m][nt], AH, bl[nt][0], bl[nt][1]);
         }
       }
     }
