@@ -270,7 +270,7 @@ namespace sr {
 // GV: also write grad T_k(y_k(p)) (interpolant gradient / spacing, zero outside the hull; the
 // values pass 2 would re-gather) as G[(k D + c) vstride + p], so pass 2 becomes a pure stream.
 template <int D, bool POW2, int SPT, bool GV>
-__global__ void __launch_bounds__(256, 8) k_sample_v(const Args a, float* __restrict__ V, float* __restrict__ G,
+__global__ void __launch_bounds__(256, SPT <= 4 ? 8 : 4) k_sample_v(const Args a, float* __restrict__ V, float* __restrict__ G,
                                                      long long vstride) {
   // grid (pixel blocks, K): block-uniform 64-bit bases, 32-bit per-thread offsets
   constexpr int BP = 256 * SPT;  // pixels per block
