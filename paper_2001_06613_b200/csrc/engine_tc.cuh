@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(256, SPT <= 4 ? 8 : 4) k_sample_v(const Args a
   const bool full = nb >= BP;
   // GV: y is read once (evict first); V and grad T are re-read by the Gram and the streaming pass 2
   // (evict last), so they should survive in L2 until then
-  const uint64_t pol_first = GV ? l2_policy_evict_first() : 0, pol_last = GV ? l2_policy_evict_last() : 0;
+  const uint64_t pol_first = GV ? l2_policy_evict_first() : 0;
   float p[SPT][D];
 #pragma unroll
   for (int e = 0; e < SPT; ++e) {
@@ -307,9 +307,17 @@ __global__ void __launch_bounds__(256, SPT <= 4 ? 8 : 4) k_sample_v(const Args a
     const int pe = tid + 256 * e;
     if (full || pe < nb) {
       if (GV) {
-        stg_hint(vb + pe, v[e] - sh, pol_last);
+        // plain stores (default L2 policy): measured faster than evict_last-hinted volatile-asm stores
+        // (34.4 vs 38.4 us at C2 — the hinted stores serialised against the gathers' scheduling)
+        if (a.dbg & 16384) {  // profiling comparison: evict_last-hinted stores
+          stg_hint(vb + pe, v[e] - sh, pol_first ^ pol_first ^ l2_policy_evict_last());
 #pragma unroll
-        for (int c = 0; c < D; ++c) stg_hint(gb + (long long)c * vstride + pe, gd[e][c], pol_last);
+          for (int c = 0; c < D; ++c) stg_hint(gb + (long long)c * vstride + pe, gd[e][c], l2_policy_evict_last());
+        } else {
+          vb[pe] = v[e] - sh;
+#pragma unroll
+          for (int c = 0; c < D; ++c) gb[(long long)c * vstride + pe] = gd[e][c];
+        }
       } else {
         vb[pe] = v[e] - sh;
       }
