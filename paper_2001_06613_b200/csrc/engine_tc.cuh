@@ -325,6 +325,65 @@ __global__ void __launch_bounds__(256, SPT <= 4 ? 8 : 4) k_sample_v(const Args a
   }
 }
 
+// k_sample_v with GV, software-pipelined over NI consecutive 1024-pixel blocks of one frame per CTA:
+// the y of block i + 1 is loaded before the gathers of block i, so only the gathers' latency is
+// exposed per block (k_sample_v exposes the y latency and then the gather latency).
+template <int D, bool POW2, int NI>
+__global__ void __launch_bounds__(256, 6) k_sample_vp(const Args a, float* __restrict__ V, float* __restrict__ G,
+                                                      long long vstride) {
+  constexpr int SPT = 4, BP = 256 * SPT;
+  const int npix = (int)(a.pix_hi - a.pix_lo);
+  const int k = (int)blockIdx.y;
+  const int tid = (int)threadIdx.x;
+  const int fi = a.job->frame_index[k];
+  const float* img = reinterpret_cast<const float*>(a.frames) + (long long)fi * a.g.N;
+  const float* yk = reinterpret_cast<const float*>(a.y) + (long long)(k * D) * a.y_stride + (a.pix_lo - a.y_off);
+  float* vk = V + (long long)k * vstride;
+  float* gk = G + (long long)(k * D) * vstride;
+  const uint64_t pol_first = l2_policy_evict_first();
+  const float* shifts = reinterpret_cast<const float*>(a.shifts);
+  const float sh = shifts ? shifts[fi] : 0.f;
+  const int bfirst = (int)blockIdx.x * NI;
+  auto load_y = [&](int blk, float (&p)[SPT][D]) {
+    const int b0 = blk * BP, nb = npix - b0;
+#pragma unroll
+    for (int e = 0; e < SPT; ++e) {
+      const int pe = b0 + min(tid + 256 * e, nb - 1);
+#pragma unroll
+      for (int c = 0; c < D; ++c) p[e][c] = ldg_hint_nv(yk + (long long)c * a.y_stride + pe, pol_first);
+    }
+  };
+  float pc[SPT][D];
+  load_y(bfirst, pc);
+#pragma unroll
+  for (int it = 0; it < NI; ++it) {
+    const int blk = bfirst + it;
+    const int b0 = blk * BP;
+    if (b0 >= npix) break;
+    float pn[SPT][D];
+    if (it + 1 < NI && b0 + BP < npix) load_y(blk + 1, pn);
+    float v[SPT], gd[SPT][D];
+#pragma unroll
+    for (int e = 0; e < SPT; ++e) v[e] = interp<float, float, D, true, POW2>(img, a.g, pc[e], gd[e]);
+    const int nb = npix - b0;
+#pragma unroll
+    for (int e = 0; e < SPT; ++e) {
+      const int pe = tid + 256 * e;
+      if (pe < nb) {
+        vk[b0 + pe] = v[e] - sh;
+#pragma unroll
+        for (int c = 0; c < D; ++c) gk[(long long)c * vstride + b0 + pe] = gd[e][c];
+      }
+    }
+    if (it + 1 < NI) {
+#pragma unroll
+      for (int e = 0; e < SPT; ++e)
+#pragma unroll
+        for (int c = 0; c < D; ++c) pc[e][c] = pn[e][c];
+    }
+  }
+}
+
 // Streaming pass 2 (fp32 NCC displacement, K <= 32) after a k_sample_v<GV = true> pass 1 on the same
 // y: block = 64 pixels x 4 frame groups; thread (pixel, group g) forms q_j = beta'_j + sum_i M'_ij V_i(p)
 // for the 8 frames j = 8 g .. 8 g + 7 (V read by the 4 group threads: L1 hits; M' broadcast from

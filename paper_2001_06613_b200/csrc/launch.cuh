@@ -287,6 +287,10 @@ cudaError_t run_pass1_split(const Launch& L, const Args& a, float* V, float* G, 
 // Split NGF path (engine_ngf.cuh).  Ranges: V / grad T over [vlo, vhi) = slab +- 2 rows, n / rho / z over
 // [zlo, zhi) = slab +- 1 row, the Gram over the slab.  cudaErrorNotSupported: layouts the TMA map cannot
 // express (the caller falls back to the generic kernels).
+// the split paths' sampling kernel launcher (mma_pass.cu)
+cudaError_t sample_vg_d2(const Launch& L, const Args& a, float* V, float* G, long long vstride);
+cudaError_t sample_vg_d3(const Launch& L, const Args& a, float* V, float* G, long long vstride);
+
 struct NgfBufs {
   float *V, *G, *Nf, *Rho, *Z;
   long long vlo, vhi, vstride, zlo, zhi, zstride;
@@ -317,11 +321,7 @@ cudaError_t run_ngf_pass1_kp(const Launch& L, const Args& a, const NgfBufs& B, d
   av.pix_lo = B.vlo;
   av.pix_hi = B.vhi;
   av.shifts = nullptr;
-  constexpr int SPT = 4;
-  const dim3 sgrid((unsigned)((B.vhi - B.vlo + 256 * SPT - 1) / (256 * SPT)), (unsigned)a.K);
-  if (a.g.pow2) k_sample_v<D, true, SPT, true><<<sgrid, 256, 0, L.stream>>>(av, B.V, B.G, B.vstride);
-  else k_sample_v<D, false, SPT, true><<<sgrid, 256, 0, L.stream>>>(av, B.V, B.G, B.vstride);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = D == 2 ? sample_vg_d2(L, av, B.V, B.G, B.vstride) : sample_vg_d3(L, av, B.V, B.G, B.vstride);
   if (e != cudaSuccess) return e;
   const dim3 fgrid((unsigned)((B.zhi - B.zlo + 1023) / 1024), (unsigned)a.K);
   k_ngf_feat4<D><<<fgrid, 256, 0, L.stream>>>(a, B.V, B.vlo, B.vstride, B.Nf, B.Rho, B.zlo, B.zhi, B.zstride);

@@ -46,6 +46,47 @@ static cudaError_t run_sample_gram(const Launch& L, const Args& a, float* V, flo
   return cudaGetLastError();
 }
 
+// Sampling kernel of the split paths (V = v - shift and grad T).  Default: k_sample_vp over 2 blocks
+// per CTA (33.0 vs 37.5 us at C2).  SEQREG_B200_SPT: 4 / 2 / 8 = k_sample_v with that many samples in
+// flight per thread, 44 = k_sample_vp over 4 blocks.
+template <int D>
+static cudaError_t launch_sample_vg(const Launch& L, const Args& a, float* V, float* G, long long vstride) {
+  const long long npix = a.pix_hi - a.pix_lo;
+  // SEQREG_B200_SPT: samples in flight per thread of k_sample_v (2, 4 or 8)
+  static const int spt = getenv("SEQREG_B200_SPT") ? atoi(getenv("SEQREG_B200_SPT")) : 42;
+  if (spt == 8) {
+    const dim3 sgrid((unsigned)((npix + 256 * 8 - 1) / (256 * 8)), (unsigned)a.K);
+    if (a.g.pow2) k_sample_v<D, true, 8, true><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
+    else k_sample_v<D, false, 8, true><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
+  } else if (spt == 2) {
+    const dim3 sgrid((unsigned)((npix + 256 * 2 - 1) / (256 * 2)), (unsigned)a.K);
+    if (a.g.pow2) k_sample_v<D, true, 2, true><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
+    else k_sample_v<D, false, 2, true><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
+  } else if (spt == 42) {  // software-pipelined over 2 blocks per CTA (k_sample_vp)
+    const long long nblk = (npix + 1023) / 1024;
+    const dim3 sgrid((unsigned)((nblk + 1) / 2), (unsigned)a.K);
+    if (a.g.pow2) k_sample_vp<D, true, 2><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
+    else k_sample_vp<D, false, 2><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
+  } else if (spt == 44) {  // ... over 4 blocks per CTA
+    const long long nblk = (npix + 1023) / 1024;
+    const dim3 sgrid((unsigned)((nblk + 3) / 4), (unsigned)a.K);
+    if (a.g.pow2) k_sample_vp<D, true, 4><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
+    else k_sample_vp<D, false, 4><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
+  } else {
+    constexpr int SPT = 4;
+    const dim3 sgrid((unsigned)((npix + 256 * SPT - 1) / (256 * SPT)), (unsigned)a.K);
+    if (a.g.pow2) k_sample_v<D, true, SPT, true><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
+    else k_sample_v<D, false, SPT, true><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
+  }
+  return cudaGetLastError();
+}
+cudaError_t sample_vg_d2(const Launch& L, const Args& a, float* V, float* G, long long vstride) {
+  return launch_sample_vg<2>(L, a, V, G, vstride);
+}
+cudaError_t sample_vg_d3(const Launch& L, const Args& a, float* V, float* G, long long vstride) {
+  return launch_sample_vg<3>(L, a, V, G, vstride);
+}
+
 // 3-D view [rows][ncomp][npix] (row stride ncomp * stride, component stride `stride` floats) for the
 // TMA-fed Gram: boxes of [32 rows x 1 component x 32 pixels], SWIZZLE_128B, zero fill past the edges
 static bool encode_gram_map(EncodeTiledFn fn, CUtensorMap* m, const float* base, long long npix, int ncomp,
@@ -76,11 +117,7 @@ static cudaError_t run_ngf_pass1_mma(const Launch& L, const Args& a, const NgfBu
   av.pix_lo = B.vlo;
   av.pix_hi = B.vhi;
   av.shifts = nullptr;
-  constexpr int SPT = 4;
-  const dim3 sgrid((unsigned)((B.vhi - B.vlo + 256 * SPT - 1) / (256 * SPT)), (unsigned)a.K);
-  if (a.g.pow2) k_sample_v<D, true, SPT, true><<<sgrid, 256, 0, L.stream>>>(av, B.V, B.G, B.vstride);
-  else k_sample_v<D, false, SPT, true><<<sgrid, 256, 0, L.stream>>>(av, B.V, B.G, B.vstride);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_sample_vg<D>(L, av, B.V, B.G, B.vstride);
   if (e != cudaSuccess) return e;
   const dim3 fgrid((unsigned)((B.zhi - B.zlo + 1023) / 1024), (unsigned)a.K);
   k_ngf_feat4<D><<<fgrid, 256, 0, L.stream>>>(a, B.V, B.vlo, B.vstride, B.Nf, B.Rho, B.zlo, B.zhi, B.zstride);
@@ -112,23 +149,7 @@ static cudaError_t run_sample_then_gram(const Launch& L, const Args& a, float* V
                                         double* part, size_t part_cap, int* nblk) {
   const long long npix = a.pix_hi - a.pix_lo;
   if (npix <= 0 || a.K > GMM::KP) return cudaErrorInvalidValue;
-  // SEQREG_B200_SPT: samples in flight per thread of k_sample_v (2, 4 or 8)
-  static const int spt = getenv("SEQREG_B200_SPT") ? atoi(getenv("SEQREG_B200_SPT")) : 4;
-  if (spt == 8) {
-    const dim3 sgrid((unsigned)((npix + 256 * 8 - 1) / (256 * 8)), (unsigned)a.K);
-    if (a.g.pow2) k_sample_v<D, true, 8, true><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
-    else k_sample_v<D, false, 8, true><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
-  } else if (spt == 2) {
-    const dim3 sgrid((unsigned)((npix + 256 * 2 - 1) / (256 * 2)), (unsigned)a.K);
-    if (a.g.pow2) k_sample_v<D, true, 2, true><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
-    else k_sample_v<D, false, 2, true><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
-  } else {
-    constexpr int SPT = 4;
-    const dim3 sgrid((unsigned)((npix + 256 * SPT - 1) / (256 * SPT)), (unsigned)a.K);
-    if (a.g.pow2) k_sample_v<D, true, SPT, true><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
-    else k_sample_v<D, false, SPT, true><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
-  }
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_sample_vg<D>(L, a, V, G, vstride);
   if (e != cudaSuccess) return e;
   const long long ntiles = (npix + GMM::TP - 1) / GMM::TP;
   const size_t stride = (size_t)GMM::KP * GMM::KP + 3 * GMM::KP;
