@@ -50,7 +50,8 @@ def kernel_bytes_per_vf(d: int, s: int) -> dict:
             "k_pass2": (1 + 2 * d) * s, "k_pass1_tc": (1 + d) * s, "k_pass1_ws": (1 + d) * s, "k_pass1": (1 + d) * s,
             "k_reduce_finalize": 0,
             # split NGF path: u -> (n, rho); Gram of n; z from (n, rho); adjoint stencil of z with grad T
-            "k_ngf_feat": (2 + d) * s, "k_gram_tcx": d * s, "k_ngf_z": (2 * d + 1) * s, "k_ngf_z_mma": (2 * d + 1) * s,
+            "k_ngf_feat": (2 + d) * s, "k_gram_tcx": d * s, "k_ngf_z": (2 * d + 1) * s, "k_ngf_z_mma": (2 * d + 1) * s, "k_ngf_z_f16": (2 * d + 1) * s,
+            "k_ngf_feat4": (2 + d) * s, "k_ngf_adj4": 3 * d * s,
             "k_ngf_adj_stream": 3 * d * s}
 
 
