@@ -723,25 +723,31 @@ __global__ void __launch_bounds__(P2M::NT, MINB) k_pass2_mma(const Args a, const
     }
     // grad T of this lane's outputs: frames 16 m + g + 8 h, pixels p0 + 4t .. + 3 (one 128-bit load)
     const int pq = p0 + 4 * t;
-    float4 gv[2][2][D];
-#pragma unroll
-    for (int m = 0; m < 2; ++m)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int j = min(16 * m + g + 8 * h, K - 1);
-#pragma unroll
-        for (int c = 0; c < D; ++c) {
-          const float* src = G + ((j * D + c) * vs + pq);
-          if (fullb && vin) {
-            gv[m][h][c] = __ldcs(reinterpret_cast<const float4*>(src));
-          } else {
-            gv[m][h][c].x = pq < npix ? src[0] : 0.f;
-            gv[m][h][c].y = pq + 1 < npix ? src[1] : 0.f;
-            gv[m][h][c].z = pq + 2 < npix ? src[2] : 0.f;
-            gv[m][h][c].w = pq + 3 < npix ? src[3] : 0.f;
-          }
-        }
+    auto load_g = [&](int m, int h, int c) {
+      const int j = min(16 * m + g + 8 * h, K - 1);
+      const float* src = G + ((j * D + c) * vs + pq);
+      float4 r;
+      if (fullb && vin) {
+        r = __ldcs(reinterpret_cast<const float4*>(src));
+      } else {
+        r.x = pq < npix ? src[0] : 0.f;
+        r.y = pq + 1 < npix ? src[1] : 0.f;
+        r.z = pq + 2 < npix ? src[2] : 0.f;
+        r.w = pq + 3 < npix ? src[3] : 0.f;
       }
+      return r;
+    };
+    // MINB <= 2: all of the step's grad T loads are issued before the MMAs (128 registers, 16 warps/SM);
+    // MINB >= 3: loaded in the epilogue (fewer registers, more warps to hide the latency)
+    float4 gv[2][2][D];
+    if constexpr (MINB <= 2) {
+#pragma unroll
+      for (int m = 0; m < 2; ++m)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int c = 0; c < D; ++c) gv[m][h][c] = load_g(m, h, c);
+    }
     float acc[2][2][4];  // [m][nt]: four independent accumulator chains (beta' + HH + LH + HL)
 #pragma unroll
     for (int m = 0; m < 2; ++m)
@@ -789,7 +795,7 @@ __global__ void __launch_bounds__(P2M::NT, MINB) k_pass2_mma(const Args a, const
 #pragma unroll
           for (int c = 0; c < D; ++c) {
             float* dst = ob + ((j * D + c) * os + pq);
-            const float4 gg = gv[m][h][c];
+            const float4 gg = MINB <= 2 ? gv[m][h][c] : load_g(m, h, c);
             const float4 r = make_float4(q0 * gg.x, q1 * gg.y, q2 * gg.z, q3 * gg.w);
             if (fullb && vout) {
               __stcs(reinterpret_cast<float4*>(dst), r);
