@@ -418,7 +418,9 @@ struct GTM {
   static constexpr int SBYTES = KP * TP * 4;          // one stage: 4 boxes of [32 rows x 128 B]
   static constexpr int ABYTES = 8 * 6 * 4 * 32 * 8;  // fp64 Gram accumulators [warp][block][r][lane]
 };
-constexpr size_t gtm_smem() { return 1024 + (size_t)GTM::NST * GTM::SBYTES + 256 + GTM::ABYTES; }
+constexpr size_t gtm_smem(int sup = 1) {
+  return 1024 + (size_t)GTM::NST * GTM::SBYTES * sup + 256 + (size_t)GTM::ABYTES * sup;
+}
 
 // hi = v with the 13 low mantissa bits cleared (exact in tf32; one LOP3 instead of the ~4-instruction
 // cvt.rna), lo = v - hi exactly (|lo| < 2^-10 |v|, truncated to tf32 by the MMA: 2^-20 relative).
@@ -432,26 +434,32 @@ __device__ __forceinline__ void split_q(const uint32_t (&q)[4], uint32_t (&h)[4]
 
 // NGF: the same Gram over the feature array n [K][ncomp][zstride] (rows = frames, columns = (component,
 // pixel) tiles of a 3-D map); the statistics slots then carry max |n| (the NGF degeneracy threshold).
-template <bool NGF>
-__global__ void __launch_bounds__(GTM::NT, 2) k_gram_tma(const Args a, const __grid_constant__ CUtensorMap vmap,
-                                                         int ntx) {
-  constexpr int KP = GTM::KP, TP = GTM::TP, NST = GTM::NST;
+// SUP: tiles per ring stage (CTA of 8 SUP warps, warp w on tile w >> 3 of the stage): SUP = 2 runs one
+// CTA of 16 warps per SM and halves the per-CTA partials the reduction reads.
+template <bool NGF, int SUP>
+__global__ void __launch_bounds__(GTM::NT * SUP, SUP == 1 ? 2 : 1) k_gram_tma(const Args a,
+                                                                             const __grid_constant__ CUtensorMap vmap,
+                                                                             int ntx) {
+  constexpr int KP = GTM::KP, TP = GTM::TP, NST = GTM::NST, NTT = GTM::NT * SUP, NW = NTT / 32;
+  constexpr int SB = GTM::SBYTES * SUP;  // one stage
   extern __shared__ __align__(1024) unsigned char gtm_sh[];
   unsigned char* base = gtm_sh + ((1024 - (smem_u32(gtm_sh) & 1023)) & 1023);
-  uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)NST * GTM::SBYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)NST * SB);
   uint64_t* empty = full + NST;
-  // fp64 accumulators in shared memory (not registers): [warp 8][block 6][r 4][lane 32]
-  double* gsm = reinterpret_cast<double*>(base + (size_t)NST * GTM::SBYTES + 256);
+  // fp64 accumulators in shared memory (not registers): [warp NW][block 6][r 4][lane 32]
+  double* gsm = reinterpret_cast<double*>(base + (size_t)NST * SB + 256);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   const int K = a.K;
   const long long npix = a.pix_hi - a.pix_lo;
   const long long ntiles = (long long)ntx * (NGF ? a.g.nd : 1);  // tile t: component t / ntx, x-tile t % ntx
-  const long long nloc = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const long long nsup = (ntiles + SUP - 1) / SUP;                // stage-sized groups of SUP tiles
+  const long long nloc = nsup > blockIdx.x ? (nsup - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const int sub = warp >> 3, wl = warp & 7;  // this warp's tile in the stage and pixel slice of it
   if (tid == 0) {
     for (int s2 = 0; s2 < NST; ++s2) {
       mbar_init(&full[s2], 1);
-      mbar_init(&empty[s2], GTM::NT / 32);
+      mbar_init(&empty[s2], NW);
     }
     fence_mbar_init();
     tma_prefetch_desc(&vmap);
@@ -459,28 +467,32 @@ __global__ void __launch_bounds__(GTM::NT, 2) k_gram_tma(const Args a, const __g
   pdl_wait();  // V of the sampling kernel
   pdl_trigger();
   __syncthreads();
-  auto issue = [&](long long n, int s2) {
-    const long long tt = blockIdx.x + n * gridDim.x;
-    const int x0 = (int)(tt % ntx) * TP, c = (int)(tt / ntx);
-    unsigned char* st = base + (size_t)s2 * GTM::SBYTES;
-    mbar_arrive_expect_tx(&full[s2], (uint32_t)GTM::SBYTES);
+  auto issue = [&](long long n, int s2) {  // tiles past the end load as zeros (out-of-range coordinates)
+    unsigned char* st = base + (size_t)s2 * SB;
+    mbar_arrive_expect_tx(&full[s2], (uint32_t)SB);
 #pragma unroll
-    for (int b = 0; b < TP / GTM::BOXP; ++b) tma_load_3d(st + b * 4096, &vmap, x0 + GTM::BOXP * b, c, 0, &full[s2]);
+    for (int u = 0; u < SUP; ++u) {
+      const long long tt = (blockIdx.x + n * gridDim.x) * SUP + u;
+      const int x0 = (int)(tt % ntx) * TP, c = (int)(tt / ntx);
+#pragma unroll
+      for (int b = 0; b < TP / GTM::BOXP; ++b)
+        tma_load_3d(st + u * GTM::SBYTES + b * 4096, &vmap, x0 + GTM::BOXP * b, c, 0, &full[s2]);
+    }
   };
   if (tid == 0)
     for (long long n = 0; n < nloc && n < NST; ++n) issue(n, (int)n);
-  // this warp's ldmatrix row addresses inside a stage: box warp >> 1, pixel columns 16 (warp & 1) + 8 kq
+  // this warp's ldmatrix row addresses inside a stage: tile sub, box wl >> 1, pixel columns 16 (wl & 1) + 8 kq
   const int lr = lane & 7, lj = lane >> 3;
   uint32_t aadr[2][2], badr[2][2];  // [m][kq], swizzled (16-byte chunk ^ (row & 7))
 #pragma unroll
   for (int m = 0; m < 2; ++m)
 #pragma unroll
     for (int kq = 0; kq < 2; ++kq) {
-      const int c = 16 * (warp & 1) + 8 * kq;
+      const int c = 16 * (wl & 1) + 8 * kq;
       const int ra = 16 * m + lr + 8 * (lj & 1), ca = c + 4 * (lj >> 1);
       const int rb = 16 * m + lr + 8 * (lj >> 1), cb = c + 4 * (lj & 1);
-      aadr[m][kq] = (uint32_t)((warp >> 1) * 4096 + ra * 128 + (((ca >> 2) ^ (ra & 7)) << 4));
-      badr[m][kq] = (uint32_t)((warp >> 1) * 4096 + rb * 128 + (((cb >> 2) ^ (rb & 7)) << 4));
+      aadr[m][kq] = (uint32_t)(sub * GTM::SBYTES + (wl >> 1) * 4096 + ra * 128 + (((ca >> 2) ^ (ra & 7)) << 4));
+      badr[m][kq] = (uint32_t)(sub * GTM::SBYTES + (wl >> 1) * 4096 + rb * 128 + (((cb >> 2) ^ (rb & 7)) << 4));
     }
   const uint32_t sb = smem_u32(base);
   float acc[6][4] = {};
@@ -498,8 +510,10 @@ __global__ void __launch_bounds__(GTM::NT, 2) k_gram_tma(const Args a, const __g
     }
   for (long long n = 0; n < nloc; ++n) {
     const int s2 = (int)(n % NST);
-    const uint32_t st = sb + (uint32_t)(s2 * GTM::SBYTES);
-    const long long p0 = ((blockIdx.x + n * gridDim.x) % ntx) * TP + 16 * warp;  // this warp's first pixel
+    const uint32_t st = sb + (uint32_t)(s2 * SB);
+    const long long tt = (blockIdx.x + n * gridDim.x) * SUP + sub;
+    // this warp's first pixel (npix for a tile past the end: every pixel masked)
+    const long long p0 = tt < ntiles ? (tt % ntx) * TP + 16 * wl : npix;
     mbar_wait(&full[s2], (uint32_t)((n / NST) & 1));
     uint32_t QA[2][2][4], QB[2][2][4];
 #pragma unroll
@@ -613,10 +627,10 @@ __global__ void __launch_bounds__(GTM::NT, 2) k_gram_tma(const Args a, const __g
     }
   __syncthreads();
   double* out = a.part + (size_t)blockIdx.x * (KP * KP + 3 * KP);
-  for (int e = tid; e < 6 * 4 * 32; e += GTM::NT) {
+  for (int e = tid; e < 6 * 4 * 32; e += NTT) {
     double v = red[e];
 #pragma unroll
-    for (int w2 = 1; w2 < 8; ++w2) v += red[w2 * 6 * 4 * 32 + e];
+    for (int w2 = 1; w2 < NW; ++w2) v += red[w2 * 6 * 4 * 32 + e];
     const int b = e >> 7, r = (e >> 5) & 3, ln = e & 31;
     const int m = b < 4 ? 0 : 1, nn = b < 4 ? b : b - 2;
     const int i = 16 * m + (ln >> 2) + 8 * (r >> 1), j = 8 * nn + 2 * (ln & 3) + (r & 1);
@@ -627,7 +641,7 @@ __global__ void __launch_bounds__(GTM::NT, 2) k_gram_tma(const Args a, const __g
     const int k = tid;
     double sv = 0.0, mx = -INFINITY, mn = INFINITY;
 #pragma unroll
-    for (int w2 = 0; w2 < 8; ++w2) {
+    for (int w2 = 0; w2 < NW; ++w2) {
       sv += rs[(w2 * 32 + k) * 3 + 0];
       mx = fmax(mx, rs[(w2 * 32 + k) * 3 + 1]);
       mn = fmin(mn, rs[(w2 * 32 + k) * 3 + 2]);

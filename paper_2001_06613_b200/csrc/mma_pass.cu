@@ -46,6 +46,12 @@ static cudaError_t run_sample_gram(const Launch& L, const Args& a, float* V, flo
   return cudaGetLastError();
 }
 
+// SEQREG_B200_GSUP: tiles per k_gram_tma ring stage (1: 2 CTAs x 8 warps per SM; 2: 1 CTA x 16 warps)
+static int gram_sup() {
+  static const int s = getenv("SEQREG_B200_GSUP") ? atoi(getenv("SEQREG_B200_GSUP")) : 1;
+  return s == 2 ? 2 : 1;
+}
+
 // Sampling kernel of the split paths (V = v - shift and grad T).  Default: k_sample_vp over 2 blocks
 // per CTA (33.0 vs 37.5 us at C2).  SEQREG_B200_SPT: 4 / 2 / 8 = k_sample_v with that many samples in
 // flight per thread, 44 = k_sample_vp over 4 blocks.
@@ -123,16 +129,18 @@ static cudaError_t run_ngf_pass1_mma(const Launch& L, const Args& a, const NgfBu
   k_ngf_feat4<D><<<fgrid, 256, 0, L.stream>>>(a, B.V, B.vlo, B.vstride, B.Nf, B.Rho, B.zlo, B.zhi, B.zstride);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const size_t smem = gtm_smem();
-  e = cudaFuncSetAttribute(k_gram_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int sup = gram_sup();
+  const size_t smem = gtm_smem(sup);
+  auto gk = sup == 2 ? k_gram_tma<true, 2> : k_gram_tma<true, 1>;
+  e = cudaFuncSetAttribute(gk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int ntx = (int)((npix + GTM::TP - 1) / GTM::TP);
-  int grid = occupancy_grid(L, k_gram_tma<true>, GTM::NT, smem, (long long)ntx * D);
+  int grid = occupancy_grid(L, gk, GTM::NT * sup, smem, ((long long)ntx * D + sup - 1) / sup);
   const size_t stride = (size_t)GTM::KP * GTM::KP + 3 * GTM::KP;
   if ((size_t)grid * stride > part_cap) grid = (int)(part_cap / stride);
   Args b = a;
   b.part = part;
-  k_gram_tma<true><<<grid, GTM::NT, smem, L.stream>>>(b, xmap, ntx);
+  gk<<<grid, GTM::NT * sup, smem, L.stream>>>(b, xmap, ntx);
   *nblk = grid;
   return cudaGetLastError();
 }
@@ -157,14 +165,16 @@ static cudaError_t run_sample_then_gram(const Launch& L, const Args& a, float* V
   if (fn && !getenv("SEQREG_B200_GRAMREG")) {  // TMA-fed Gram (k_gram_tma)
     CUtensorMap vmap;
     if (encode_gram_map(fn, &vmap, V, npix, 1, a.K, vstride)) {
-      const size_t smem = gtm_smem();
-      e = cudaFuncSetAttribute(k_gram_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      const int sup = gram_sup();
+      const size_t smem = gtm_smem(sup);
+      auto gk = sup == 2 ? k_gram_tma<false, 2> : k_gram_tma<false, 1>;
+      e = cudaFuncSetAttribute(gk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
-      int grid = occupancy_grid(L, k_gram_tma<false>, GTM::NT, smem, ntiles);
+      int grid = occupancy_grid(L, gk, GTM::NT * sup, smem, (ntiles + sup - 1) / sup);
       if ((size_t)grid * stride > part_cap) grid = (int)(part_cap / stride);
       Args b = a;
       b.part = part;
-      e = launch_pdl(k_gram_tma<false>, dim3(grid), dim3(GTM::NT), smem, L.stream, b, vmap, (int)ntiles);
+      e = launch_pdl(gk, dim3(grid), dim3(GTM::NT * sup), smem, L.stream, b, vmap, (int)ntiles);
       *nblk = grid;
       return e;
     }

@@ -48,6 +48,14 @@ def main():
 
     plan.corr_partial(prob)
     from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA]) as prof0:
+        for _ in range(20):
+            plan.corr_partial(prob)  # reduce only (no finalize)
+        torch.cuda.synchronize()
+    for ev in prof0.events():
+        if ev.device_type.name == "CUDA" and "reduce" in ev.name:
+            print(f"  reduce only: {ev.name.split('(')[0][-40:]} {ev.device_time:.2f} us")
+            break
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         for _ in range(20):
             plan.finalize(prob, w, grid.cell_volume)
