@@ -45,7 +45,7 @@ def bytes_per_vf(d: int, s: int) -> dict:
 # reads them back and writes dD/dy; the fused kernels move exactly the SURVEY §8d pass figures
 def kernel_bytes_per_vf(d: int, s: int) -> dict:
     return {"k_sample_v": 2 * (1 + d) * s, "k_gram_tc": s, "k_pass2_stream": (1 + 2 * d) * s,
-            "k_sample_gram": 2 * (1 + d) * s, "k_sample_vp": 2 * (1 + d) * s, "k_pass2_mma": (1 + 2 * d) * s, "k_gram_tma": s, "k_gram_mma": s,
+            "k_sample_gram": 2 * (1 + d) * s, "k_sample_vp": 2 * (1 + d) * s, "k_pass2_tma": (1 + 2 * d) * s, "k_pass2_mma": (1 + 2 * d) * s, "k_gram_tma": s, "k_gram_mma": s,
             "k_pass2_bulk": (1 + 2 * d) * s,
             "k_pass2": (1 + 2 * d) * s, "k_pass1_tc": (1 + d) * s, "k_pass1_ws": (1 + d) * s, "k_pass1": (1 + d) * s,
             "k_reduce_finalize": 0,

@@ -826,6 +826,186 @@ __global__ void __launch_bounds__(P2M::NT, MINB) k_pass2_mma(const Args a, const
 }
 
 
+// Pass 2, TMA-fed (fp32 NCC displacement, K <= 32): the math and lane layout of k_pass2_mma, but the
+// tile's V rows ([32 frames x 128 pixels]) and grad T rows ([32 D rows x 128 pixels]) arrive by 3-D TMA
+// (SWIZZLE_128B boxes of 32 pixels, zero fill past K and past the slab) into a 2-stage ring, so the next
+// tile is in flight while this one is contracted and no register holds in-flight data.
+template <int D>
+struct P2T {
+  static constexpr int NT = 256, TP = 128, NST = 2;
+  static constexpr int VB = 32 * 32 * 4, GB = 32 * D * 32 * 4;     // one V box, one grad T box
+  static constexpr int SBYTES = 4 * VB + 4 * GB;                    // one stage
+  static constexpr size_t smem() { return 1024 + (size_t)NST * SBYTES + 256 + 2 * 2 * 4 * 32 * 16; }
+};
+
+template <int D>
+__global__ void __launch_bounds__(P2T<D>::NT, D == 2 ? 2 : 1) k_pass2_tma(const Args a, const __grid_constant__ CUtensorMap vmap,
+                                                            const __grid_constant__ CUtensorMap gmap) {
+  using C = P2T<D>;
+  constexpr int NST = C::NST, TP = C::TP;
+  extern __shared__ __align__(1024) unsigned char p2t_sh[];
+  unsigned char* base = p2t_sh + ((1024 - (smem_u32(p2t_sh) & 1023)) & 1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)NST * C::SBYTES);
+  uint64_t* empty = full + NST;
+  float4* Ah = reinterpret_cast<float4*>(base + (size_t)NST * C::SBYTES + 256);  // [m 2][ks 4][lane 32]
+  float4* Al = Ah + 2 * 4 * 32;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int K = a.K;
+  const StatsLayout L(K);
+  const double* Md = a.stats + L.M;
+  const int npix = (int)(a.pix_hi - a.pix_lo);
+  const int ntiles = (npix + TP - 1) / TP;
+  const int nloc = ntiles > (int)blockIdx.x ? (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+  if (tid == 0) {
+    for (int s2 = 0; s2 < NST; ++s2) {
+      mbar_init(&full[s2], 1);
+      mbar_init(&empty[s2], C::NT / 32);
+    }
+    fence_mbar_init();
+    tma_prefetch_desc(&vmap);
+    tma_prefetch_desc(&gmap);
+  }
+  auto issue = [&](int n, int s2) {
+    const int x0 = ((int)blockIdx.x + n * (int)gridDim.x) * TP;
+    unsigned char* st = base + (size_t)s2 * C::SBYTES;
+    mbar_arrive_expect_tx(&full[s2], (uint32_t)C::SBYTES);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      tma_load_3d(st + b * C::VB, &vmap, x0 + 32 * b, 0, 0, &full[s2]);
+      tma_load_3d(st + 4 * C::VB + b * C::GB, &gmap, x0 + 32 * b, 0, 0, &full[s2]);
+    }
+  };
+  for (int e = tid; e < 2 * 4 * 32; e += C::NT) {
+    const int m = e >> 7, ks = (e >> 5) & 3, ln = e & 31;
+    const int gg = ln >> 2, tt = ln & 3;
+    float hv[4], lv[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {  // A[j][i] = M'[i][j]
+      const int j = 16 * m + gg + 8 * (r & 1), i = 8 * ks + tt + 4 * (r >> 1);
+      const double mv = (i < K && j < K) ? Md[i * K + j] : 0.0;
+      hv[r] = to_tf32((float)mv);
+      lv[r] = (float)(mv - (double)hv[r]);
+    }
+    Ah[e] = make_float4(hv[0], hv[1], hv[2], hv[3]);
+    Al[e] = make_float4(lv[0], lv[1], lv[2], lv[3]);
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int n = 0; n < nloc && n < NST; ++n) issue(n, n);
+  float bet[2][2];
+#pragma unroll
+  for (int m = 0; m < 2; ++m)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = 16 * m + g + 8 * h;
+      bet[m][h] = j < K ? (float)a.stats[L.beta + j] : 0.f;
+    }
+  const int os = (int)a.o_stride;
+  float* __restrict__ ob = reinterpret_cast<float*>(a.out) + (a.pix_lo - a.o_off);
+  const bool vout = (os & 3) == 0 && (reinterpret_cast<uintptr_t>(ob) & 15) == 0;
+  const int bx = warp >> 1, half = warp & 1;  // this warp's box and 16-pixel half of it
+  const int pq_in = 16 * half + 4 * t;        // this lane's first output pixel inside the box
+  for (int n = 0; n < nloc; ++n) {
+    const int s2 = n % NST;
+    const unsigned char* st = base + (size_t)s2 * C::SBYTES;
+    const unsigned char* vbx = st + bx * C::VB;
+    const unsigned char* gbx = st + 4 * C::VB + bx * C::GB;
+    const int p0 = ((int)blockIdx.x + n * (int)gridDim.x) * TP + 16 * warp;  // this warp's first pixel
+    mbar_wait(&full[s2], (uint32_t)((n / NST) & 1));
+    // B fragments: V[8 ks + t + 4u][pixel(g, nt)], pixel(g, nt) = 4 (g >> 1) + 2 nt + (g & 1)
+    float bv[4][2][2];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      const int px = 16 * half + 4 * (g >> 1) + 2 * nt + (g & 1);
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int r = 8 * ks + t + 4 * u;
+          bv[ks][nt][u] = *reinterpret_cast<const float*>(vbx + r * 128 + ((((px >> 2) ^ (r & 7))) << 4) + (px & 3) * 4);
+        }
+    }
+    // grad T rows (16 m + g + 8 h) D + c, pixels pq_in .. + 3 of the box
+    float4 gv[2][2][D];
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          const int r = (16 * m + g + 8 * h) * D + c;
+          gv[m][h][c] = *reinterpret_cast<const float4*>(gbx + r * 128 + ((((pq_in >> 2) ^ (r & 7))) << 4));
+        }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s2]);
+    if (tid == 0 && n + NST < nloc) {  // refill once every warp has read the stage
+      mbar_wait(&empty[s2], (uint32_t)((n / NST) & 1));
+      issue(n + NST, s2);
+    }
+    float acc[2][2][4];
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        acc[m][nt][0] = acc[m][nt][1] = bet[m][0];
+        acc[m][nt][2] = acc[m][nt][3] = bet[m][1];
+      }
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      uint32_t bh[2][2], bl[2][2];
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          bh[nt][u] = __float_as_uint(bv[ks][nt][u]) & 0xffffe000u;
+          bl[nt][u] = __float_as_uint(bv[ks][nt][u] - __uint_as_float(bh[nt][u]));
+        }
+      uint32_t AH[2][4], AL[2][4];
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        const float4 ah = Ah[(m * 4 + ks) * 32 + lane], al = Al[(m * 4 + ks) * 32 + lane];
+        AH[m][0] = __float_as_uint(ah.x), AH[m][1] = __float_as_uint(ah.y);
+        AH[m][2] = __float_as_uint(ah.z), AH[m][3] = __float_as_uint(ah.w);
+        AL[m][0] = __float_as_uint(al.x), AL[m][1] = __float_as_uint(al.y);
+        AL[m][2] = __float_as_uint(al.z), AL[m][3] = __float_as_uint(al.w);
+      }
+#pragma unroll
+      for (int mn = 0; mn < 4; ++mn) mma_tf32(acc[mn >> 1][mn & 1], AH[mn >> 1], bh[mn & 1][0], bh[mn & 1][1]);
+#pragma unroll
+      for (int mn = 0; mn < 4; ++mn) mma_tf32(acc[mn >> 1][mn & 1], AL[mn >> 1], bh[mn & 1][0], bh[mn & 1][1]);
+#pragma unroll
+      for (int mn = 0; mn < 4; ++mn) mma_tf32(acc[mn >> 1][mn & 1], AH[mn >> 1], bl[mn & 1][0], bl[mn & 1][1]);
+    }
+    const int pq = p0 + 4 * t;
+    const bool fullb = p0 + 16 <= npix;
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = 16 * m + g + 8 * h;
+        if (j < K) {
+          const float q0 = acc[m][0][2 * h], q1 = acc[m][0][2 * h + 1];
+          const float q2 = acc[m][1][2 * h], q3 = acc[m][1][2 * h + 1];
+#pragma unroll
+          for (int c = 0; c < D; ++c) {
+            float* dst = ob + ((j * D + c) * os + pq);
+            const float4 gg = gv[m][h][c];
+            const float4 r = make_float4(q0 * gg.x, q1 * gg.y, q2 * gg.z, q3 * gg.w);
+            if (fullb && vout) {
+              __stcs(reinterpret_cast<float4*>(dst), r);
+            } else {
+              if (pq < npix) __stcs(dst, r.x);
+              if (pq + 1 < npix) __stcs(dst + 1, r.y);
+              if (pq + 2 < npix) __stcs(dst + 2, r.z);
+              if (pq + 3 < npix) __stcs(dst + 3, r.w);
+            }
+          }
+        }
+      }
+  }
+}
+
 // Pass 2, bulk-copy pipelined (default): the same warp-level math as k_pass2_mma, but each warp streams
 // its 32-pixel blocks through two private shared-memory stages filled by 1-D bulk copies
 // (cp.async.bulk, one 128-byte row per lane: V rows, grad T rows), completion on a per-stage mbarrier;

@@ -108,6 +108,21 @@ static bool encode_gram_map(EncodeTiledFn fn, CUtensorMap* m, const float* base,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// grad T [K][D][stride] as a 3-D map for k_pass2_tma: boxes of [32 frames x D components x 32 pixels]
+template <int D>
+static bool encode_p2g_map(EncodeTiledFn fn, CUtensorMap* m, const float* base, long long npix, int rows,
+                           long long stride) {
+  memset(m, 0, sizeof *m);
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (stride * 4) % 16) return false;
+  cuuint64_t gdim[3] = {(cuuint64_t)npix, (cuuint64_t)D, (cuuint64_t)rows};
+  cuuint64_t gstr[2] = {(cuuint64_t)stride * 4, (cuuint64_t)D * stride * 4};
+  cuuint32_t box[3] = {32, (cuuint32_t)D, 32};
+  cuuint32_t es[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), gdim, gstr, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // split NGF pass 1 for K <= 32: sampling, features, then the TMA-fed mma.sync Gram of n (KP = 32 partials)
 template <int D>
 static cudaError_t run_ngf_pass1_mma(const Launch& L, const Args& a, const NgfBufs& B, double* part,
@@ -195,6 +210,21 @@ template <int D>
 static cudaError_t run_pass2_mma(const Launch& L, const Args& a, const float* V, const float* G, long long vstride) {
   const long long npix = a.pix_hi - a.pix_lo;
   if (npix <= 0) return cudaSuccess;
+  // TMA-fed pass 2 (k_pass2_tma; 24.8 vs 26.1 us at C2); SEQREG_B200_P2TMA=0: k_pass2_mma
+  static const bool p2tma = !(getenv("SEQREG_B200_P2TMA") && getenv("SEQREG_B200_P2TMA")[0] == '0');
+  EncodeTiledFn fn = encode_tiled_fn();
+  if (p2tma && fn) {
+    CUtensorMap vmap, gmap;
+    if (encode_gram_map(fn, &vmap, V, npix, 1, a.K, vstride) && encode_p2g_map<D>(fn, &gmap, G, npix, a.K, vstride)) {
+      using C = P2T<D>;
+      const size_t smem = C::smem();
+      cudaError_t e = cudaFuncSetAttribute(k_pass2_tma<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      const int grid = occupancy_grid(L, k_pass2_tma<D>, C::NT, smem, (npix + C::TP - 1) / C::TP);
+      k_pass2_tma<D><<<grid, C::NT, smem, L.stream>>>(a, vmap, gmap);
+      return cudaGetLastError();
+    }
+  }
   if (getenv("SEQREG_B200_P2BULK") && (vstride & 3) == 0 && (reinterpret_cast<uintptr_t>(V) & 15) == 0 &&
       (reinterpret_cast<uintptr_t>(G) & 15) == 0) {
     using C = P2B<D>;

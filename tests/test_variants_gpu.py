@@ -8,6 +8,8 @@ oracle's D and dD/dy: each variant runs the fp32 field parity cases in a fresh p
     SEQREG_B200_SPLIT=0   fused tcgen05 pass 1 (default: sampling kernel + tcgen05 Gram kernel)
     SEQREG_B200_GRAPH=0   no CUDA-graph replay of repeated sr_evaluate calls
     SEQREG_B200_NGFZ=2    NGF z contraction with tf32 operands (default f16); =0: the SIMT k_ngf_z
+    SEQREG_B200_P2TMA=0   pass 2 loads straight from HBM (k_pass2_mma; default TMA-fed k_pass2_tma)
+    SEQREG_B200_SPT=4     the unpipelined sampler k_sample_v (default k_sample_vp)
     SEQREG_B200_MMA=0     k_sample_v + k_gram_tc + k_pass2_stream (default: k_sample_gram + k_pass2_mma)
     SEQREG_B200_WS2=1     warp-specialized SIMT pass 2
 """
@@ -67,7 +69,7 @@ print(json.dumps(out))
 
 
 @pytest.mark.parametrize("env", ["SEQREG_B200_LEGACY=1", "SEQREG_B200_TC=0", "SEQREG_B200_TC2=1", "SEQREG_B200_P2S=0",
-                                 "SEQREG_B200_SPLIT=0", "SEQREG_B200_WS2=1", "SEQREG_B200_MMA=0", "SEQREG_B200_GRAPH=0", "SEQREG_B200_NGFZ=2", "SEQREG_B200_NGFZ=0", ""])
+                                 "SEQREG_B200_SPLIT=0", "SEQREG_B200_WS2=1", "SEQREG_B200_MMA=0", "SEQREG_B200_GRAPH=0", "SEQREG_B200_NGFZ=2", "SEQREG_B200_NGFZ=0", "SEQREG_B200_P2TMA=0", "SEQREG_B200_SPT=4", ""])
 def test_variant_parity(env):
     e = dict(os.environ)
     if env:
