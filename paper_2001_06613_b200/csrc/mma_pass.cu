@@ -213,7 +213,7 @@ static cudaError_t run_pass2_mma(const Launch& L, const Args& a, const float* V,
   // TMA-fed pass 2 (k_pass2_tma; 24.8 vs 26.1 us at C2); SEQREG_B200_P2TMA=0: k_pass2_mma
   static const bool p2tma = !(getenv("SEQREG_B200_P2TMA") && getenv("SEQREG_B200_P2TMA")[0] == '0');
   EncodeTiledFn fn = encode_tiled_fn();
-  if (p2tma && fn) {
+  if (p2tma && fn && D == 2) {  // (3-D: 152 registers, one 8-warp CTA per SM — not measured faster)
     CUtensorMap vmap, gmap;
     if (encode_gram_map(fn, &vmap, V, npix, 1, a.K, vstride) && encode_p2g_map<D>(fn, &gmap, G, npix, a.K, vstride)) {
       using C = P2T<D>;
