@@ -1315,7 +1315,7 @@ __global__ void __launch_bounds__(NZ<D>::NT, 1) k_ngf_z_mma(const Args a, const 
             float dot = 0.f;
 #pragma unroll
             for (int c = 0; c < D; ++c) dot += n[c][u] * r[c][u];
-            const float ir = 1.f / rho[u];
+            const float ir = __frcp_rn(rho[u]);  // = 1.f / rho, correctly rounded, without the division sequence
 #pragma unroll
             for (int c = 0; c < D; ++c) zz[c][u] = (r[c][u] - n[c][u] * dot) * ir;
           }
@@ -1502,7 +1502,7 @@ __global__ void __launch_bounds__(NZ<D>::NT, 1) k_ngf_z_f16(const Args a, const 
             float dot = 0.f;
 #pragma unroll
             for (int c = 0; c < D; ++c) dot += n[c][u] * r[c][u];
-            const float ir = 1.f / rho[u];
+            const float ir = __frcp_rn(rho[u]);  // = 1.f / rho, correctly rounded, without the division sequence
 #pragma unroll
             for (int c = 0; c < D; ++c) zz[c][u] = (r[c][u] - n[c][u] * dot) * ir;
           }

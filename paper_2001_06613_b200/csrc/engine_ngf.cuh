@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(256) k_ngf_feat4(const Args a, const float* __
       pn += g[ax] * g[ax];
     }
     const float rho = sqrtf(pn + e * e);
-    const float ir = 1.f / rho;
+    const float ir = __frcp_rn(rho);  // = 1.f / rho (correctly rounded)
 #pragma unroll
     for (int ax = 0; ax < D; ++ax) nv[ax][t] = g[ax] * ir;
     rv[t] = rho;
