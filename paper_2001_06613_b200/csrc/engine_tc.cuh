@@ -328,10 +328,10 @@ __global__ void __launch_bounds__(256, SPT <= 4 ? 8 : 4) k_sample_v(const Args a
 // k_sample_v with GV, software-pipelined over NI consecutive 1024-pixel blocks of one frame per CTA:
 // the y of block i + 1 is loaded before the gathers of block i, so only the gathers' latency is
 // exposed per block (k_sample_v exposes the y latency and then the gather latency).
-template <int D, bool POW2, int NI>
+template <int D, bool POW2, int NI, int SPT = 4>
 __global__ void __launch_bounds__(256, 6) k_sample_vp(const Args a, float* __restrict__ V, float* __restrict__ G,
                                                       long long vstride) {
-  constexpr int SPT = 4, BP = 256 * SPT;
+  constexpr int BP = 256 * SPT;
   const int npix = (int)(a.pix_hi - a.pix_lo);
   const int k = (int)blockIdx.y;
   const int tid = (int)threadIdx.x;

@@ -73,6 +73,16 @@ static cudaError_t launch_sample_vg(const Launch& L, const Args& a, float* V, fl
     const dim3 sgrid((unsigned)((nblk + 1) / 2), (unsigned)a.K);
     if (a.g.pow2) k_sample_vp<D, true, 2><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
     else k_sample_vp<D, false, 2><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
+  } else if (spt == 43) {  // ... over 3 blocks per CTA
+    const long long nblk = (npix + 1023) / 1024;
+    const dim3 sgrid((unsigned)((nblk + 2) / 3), (unsigned)a.K);
+    if (a.g.pow2) k_sample_vp<D, true, 3><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
+    else k_sample_vp<D, false, 3><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
+  } else if (spt == 24) {  // 4 blocks of 512 pixels per CTA, 2 samples per thread per block
+    const long long nblk = (npix + 511) / 512;
+    const dim3 sgrid((unsigned)((nblk + 3) / 4), (unsigned)a.K);
+    if (a.g.pow2) k_sample_vp<D, true, 4, 2><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
+    else k_sample_vp<D, false, 4, 2><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
   } else if (spt == 44) {  // ... over 4 blocks per CTA
     const long long nblk = (npix + 1023) / 1024;
     const dim3 sgrid((unsigned)((nblk + 3) / 4), (unsigned)a.K);
