@@ -294,6 +294,53 @@ def test_slab_sharding_sums_to_whole(feature):
     assert _relmax(gs.cpu().numpy(), g.cpu().numpy()) < 1e-12
 
 
+@pytest.mark.parametrize("reuse", [False, True])
+@pytest.mark.parametrize("feature", ["ncc", "ngf"])
+@pytest.mark.parametrize("dims", [(40, 24), (37, 26)])
+def test_slab_sharding_fp32_tensor_core_path(feature, dims, reuse):
+    """The fp32 K <= 32 split path (pipelined sampler, TMA-fed Gram, TMA-fed pass 2 / NGF z) on pixel
+    slabs — including slab starts that are not 16-byte aligned — reduces to the whole-grid evaluation
+    (fp32: summation order differs, 1e-4)."""
+    rng = np.random.default_rng(22)
+    K = 12
+    frames, spacing, origin, y, w = _random_problem(rng, dims, K)
+    h = float(np.prod(spacing))
+    fd = _frames_dev(frames, dims, spacing, origin, torch.float32)
+    whole = srb.FieldObjective(fd, list(range(K)), w, h, feature=feature, ngf_eps=0.2)
+    yt = torch.as_tensor(y, dtype=torch.float32, device=fd.data.device).contiguous()
+    stats, g = whole.evaluate(yt)
+    N = int(np.prod(dims))
+    row = dims[0]
+    cuts = [0, 7 * row, 16 * row, N]
+    raws, plans = [], []
+    for lo, hi in zip(cuts[:-1], cuts[1:]):
+        plan = srb.EvalPlan(fd, list(range(K)), feature=feature, ngf_eps=0.2, pix_range=(lo, hi))
+        prob = plan.problem(y=yt)
+        raws.append(plan.corr_partial(prob).clone())
+        plans.append((plan, prob, lo, hi))
+    total = sum(raws)
+    ext = torch.stack([r[K * K + K:K * K + 3 * K] for r in raws]).amax(0)
+    total[K * K + K:K * K + 3 * K] = ext
+    assert int(total[-1].item()) == N
+    gs = torch.zeros_like(yt)
+    eng = fd.engine
+    if reuse:  # the per-rank flow of parallel.py: pass 1 of the slab, then pass 2 streams its samples
+        eng.set_sample_reuse(True)
+    try:
+        for plan, prob, lo, hi in plans:
+            if reuse:
+                plan.corr_partial(prob)  # this slab's samples in the engine's buffers
+            plan.raw.copy_(total)
+            plan.finalize(prob, w, h, n_total=N)
+            assert float(plan.stats[0].item()) == pytest.approx(float(stats[0].item()), rel=1e-4)
+            out = torch.empty((K, 2, hi - lo), dtype=yt.dtype, device=yt.device)
+            plan.grad(prob, out, g_off=lo)
+            gs[:, :, lo:hi] = out
+    finally:
+        eng.set_sample_reuse(False)
+    assert _relmax(gs.double().cpu().numpy(), g.double().cpu().numpy()) < 1e-4
+
+
 def test_deterministic_bitwise():
     rng = np.random.default_rng(5)
     frames, spacing, origin, y, w = _random_problem(rng, (64, 48), 10)
