@@ -67,6 +67,45 @@ __global__ void __launch_bounds__(256) k_ngf_feat4(const Args a, const float* __
   coords_flat(a.g, p0, c);
   const float e = (float)a.eps;
   float nv[D][4], rv[4];
+  // interior fast path: the 4 pixels share their row and every axis index stays in 1 .. n - 2 (central
+  // differences everywhere); the u rows come as 128-bit loads
+  // (2-D only: with 128-pixel 3-D rows every warp holds a boundary thread and would run both paths)
+  bool inner = D == 2 && q0 + 4 <= nz && c[0] >= 1 && c[0] + 3 <= a.g.n[0] - 2 && ((zlo - vlo + q0) & 3) == 0 &&
+               (vstride & 3) == 0 && (reinterpret_cast<uintptr_t>(V) & 15) == 0;
+#pragma unroll
+  for (int ax = 1; ax < D; ++ax) inner = inner && c[ax] >= 1 && c[ax] <= a.g.n[ax] - 2 && (a.g.sti[ax] & 3) == 0;
+  if (inner) {
+    float g4[D][4];
+#pragma unroll
+    for (int ax = 0; ax < D; ++ax) {
+      float um[4], up[4];
+      if (ax == 0) {
+        const float4 u0 = __ldg(reinterpret_cast<const float4*>(u + q0));
+        um[0] = __ldg(u + q0 - 1), um[1] = u0.x, um[2] = u0.y, um[3] = u0.z;
+        up[0] = u0.y, up[1] = u0.z, up[2] = u0.w, up[3] = __ldg(u + q0 + 4);
+      } else {
+        const int st = a.g.sti[ax];
+        const float4 m4 = __ldg(reinterpret_cast<const float4*>(u + q0 - st));
+        const float4 p4 = __ldg(reinterpret_cast<const float4*>(u + q0 + st));
+        um[0] = m4.x, um[1] = m4.y, um[2] = m4.z, um[3] = m4.w;
+        up[0] = p4.x, up[1] = p4.y, up[2] = p4.z, up[3] = p4.w;
+      }
+      const float inv = a.g.invf[ax];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) g4[ax][t] = (up[t] - um[t]) * (inv * 0.5f);
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      float pn = 0.f;
+#pragma unroll
+      for (int ax = 0; ax < D; ++ax) pn += g4[ax][t] * g4[ax][t];
+      const float rho = sqrtf(pn + e * e);
+      const float ir = 1.f / rho;
+#pragma unroll
+      for (int ax = 0; ax < D; ++ax) nv[ax][t] = g4[ax][t] * ir;
+      rv[t] = rho;
+    }
+  } else
 #pragma unroll
   for (int t = 0; t < 4; ++t) {
     const int q = q0 + t;
@@ -123,6 +162,40 @@ __global__ void __launch_bounds__(256) k_ngf_adj4(const Args a, const float* __r
   int c[3];
   coords_flat(a.g, p0, c);
   float du[4];
+  // interior fast path: the 4 pixels share their row and every axis index stays in 2 .. n - 3, so
+  // (D_h^T z)(p) = sum_ax (z[p - st] - z[p + st]) h / 2; the z rows come as 128-bit loads
+  // (2-D only, as in k_ngf_feat4)
+  bool inner = D == 2 && q0 + 4 <= npix && c[0] >= 2 && c[0] + 3 <= a.g.n[0] - 3 && ((p0 - zlo) & 3) == 0 &&
+               (zstride & 3) == 0 && (reinterpret_cast<uintptr_t>(Z) & 15) == 0;
+#pragma unroll
+  for (int ax = 1; ax < D; ++ax) inner = inner && c[ax] >= 2 && c[ax] <= a.g.n[ax] - 3 && (a.g.sti[ax] & 3) == 0;
+  if (inner) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) du[t] = 0.f;
+#pragma unroll
+    for (int ax = 0; ax < D; ++ax) {
+      const float* z = Z + ((long long)k * D + ax) * zstride + (p0 - zlo);
+      const float h2 = a.g.invf[ax] * 0.5f;
+      float zm[4], zp[4];
+      if (ax == 0) {
+        const float4 z0 = __ldg(reinterpret_cast<const float4*>(z));
+        zm[0] = __ldg(z - 1), zm[1] = z0.x, zm[2] = z0.y, zm[3] = z0.z;
+        zp[0] = z0.y, zp[1] = z0.z, zp[2] = z0.w, zp[3] = __ldg(z + 4);
+      } else {
+        const int st = a.g.sti[ax];
+        const float4 m4 = __ldg(reinterpret_cast<const float4*>(z - st)), p4 = __ldg(reinterpret_cast<const float4*>(z + st));
+        zm[0] = m4.x, zm[1] = m4.y, zm[2] = m4.z, zm[3] = m4.w;
+        zp[0] = p4.x, zp[1] = p4.y, zp[2] = p4.z, zp[3] = p4.w;
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        float o = 0.f;  // the general path's expression order
+        o += zm[t] * h2;
+        o -= zp[t] * h2;
+        du[t] += o;
+      }
+    }
+  } else
 #pragma unroll
   for (int t = 0; t < 4; ++t) {
     float acc = 0.f;
