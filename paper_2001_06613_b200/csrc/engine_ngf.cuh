@@ -259,7 +259,9 @@ struct TGX {
   static constexpr int KP = KP_;
   static constexpr int NSP = 512, NT = NSP + 32 + 128;
   static constexpr int TP = KP == 64 ? 64 : 32;  // columns per tile (shared-memory bound at KP = 128)
-  static constexpr int NST = 2, NB = 2, NA = 2, R = 4;
+  // R tiles accumulate in a TMEM slot (fp32, 512 columns) between fp64 flushes: the flush of a
+  // 128 x N slot, not the MMAs, bounds this kernel (R = 4 -> 16 at KP = 128: 0.71 -> 0.45 ms at C3)
+  static constexpr int NST = 2, NB = 2, NA = 2, R = KP == 64 ? 8 : 16;
   static constexpr int N = KP;                   // MMA N and TMEM columns per slot
   static constexpr int SBYTES = KP * TP * 4;     // fp32 stage [KP][32]
   static constexpr int OBYTES = 128 * TP * 4;    // one 128-row operand tile (TP / 32 column atoms of 16 KB)
