@@ -267,6 +267,19 @@ static cudaError_t run_ngf_z_mma(const Launch& L, const Args& a, const NgfBufs& 
   const long long items = (nzp + C::PW - 1) / C::PW * ((JT + C::MW - 1) / C::MW);
   // SEQREG_B200_NGFZ=2: tf32 operands (k_ngf_z_mma); default f16 operands (k_ngf_z_f16)
   static const bool tf32 = getenv("SEQREG_B200_NGFZ") && getenv("SEQREG_B200_NGFZ")[0] == '2';
+  // SEQREG_B200_NGFZN=1: 8-pixel items with every m-tile (k_ngf_z_f16n), for K <= 128 (2-D: MT = JT)
+  static const bool narrow = getenv("SEQREG_B200_NGFZN") && getenv("SEQREG_B200_NGFZN")[0] == '1';
+  if (!tf32 && narrow && D == 2 && JT > C::MW) {
+    const int KS = (K + 15) / 16;
+    const size_t smem = (size_t)2 * JT * KS * 32 * 16;
+    auto kern = JT <= 6 ? k_ngf_z_f16n<D, 6> : k_ngf_z_f16n<D, 8>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const long long nblk8 = (nzp + 7) / 8;
+    const int grid = occupancy_grid(L, kern, 512, smem, (nblk8 + 15) / 16);
+    kern<<<grid, 512, smem, L.stream>>>(a, B.Nf, B.Rho, B.zlo, B.zhi, B.zstride, B.Z);
+    return cudaGetLastError();
+  }
   if (!tf32) {
     const int KS = (K + 15) / 16;
     const size_t smem = (size_t)2 * JT * KS * 32 * 16;
