@@ -1,20 +1,27 @@
 """Benchmark: voxel-frames/s of one D(y) + grad D(y) evaluation (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl reference]
 
-A step is one objective evaluation (pass 1 warp+feature+Gram, fixed-order reduce,
-finalize, pass 2 re-warp+coefficient contraction+chain rule) over the whole
-workload with inputs resident in HBM.  Default workload: BASELINE.json configs[1]
-("c2": 2-D, K=32, 512x512 float32, NCC, displacement-field iterate).  The inputs
-(frames 33.5 MB + y 67 MB) fit in the 126 MB L2, so L2 is flushed (a 256 MiB write)
-before every timed step, outside the step's CUDA-event window.
+A step is one objective evaluation (pass 1: warp + feature + Gram; fixed-order reduce + finalize;
+pass 2: re-warp + coefficient contraction + adjoint + chain rule) over the whole workload with the
+inputs resident in HBM.  Default workload: configs[2] ("c3": 2-D, K = 100, 1024 x 1024 float32, NGF,
+the largest single-GPU configuration, the one north_star names for 1/2/4/8 GPUs).  The same run also
+measures c4 (3-D, K = 20, 128^3, NGF) and c2 (configs[1], K = 32, 512^2, NCC) and reports them under
+"other_configs".  Inputs of every config are the seeded synthetic sequence (synth.make_sequence) and the
+bench iterate (synth.bench_iterate: y = x + G_(4 px) * N(0, 0.5 px), the iterate every arm and the
+full-size parity fixtures use).  c3 / c4 inputs (1.3 GB / 0.5 GB) exceed the 126 MB L2; every timed step
+is still preceded by a 256 MiB write + 256 MiB read outside the event window (c2's inputs fit in L2).
 
-Multi-GPU (torchrun, one rank per GPU, NCCL): weak scaling — every rank owns a
-512-row slab of a 512 x (512 N) domain (same per-GPU work), the K x K raw Gram sums
-are all-reduced (the only collective), and each rank assembles its slab's gradient.
+--gpus N (N > 1): re-launches itself under torch.distributed.run (one rank per GPU, NCCL) unless already
+inside a torchrun.  Strong scaling: the fixed config domain is cut into N slabs of the slowest axis
+(pixels; frames replicated), the ranks' raw K x K Gram sums are combined by one all-gather (the only
+collective), and each rank assembles its slab's gradient; value = all voxel-frames / max-over-ranks time.
 
---impl reference: the CPU oracle port of the reference path (oracle/seqreg_oracle.py,
-numpy, the reference's per-frame thread pool) on this host's cores, same metric.
+--impl reference: the CPU restatement of the reference path (oracle/seqreg_oracle.py, numpy, the
+reference's per-frame thread pool; the reference itself has neither NGF nor displacement fields) on all
+host cores, on a bounded sample of the same config (a subset of the frames at full resolution).
+
+--dry-run: no GPU work; checks the rank plumbing (gloo) and prints the line skeleton (CPU test).
 """
 
 from __future__ import annotations
@@ -22,7 +29,9 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -34,25 +43,28 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "voxel-frames/s for D(y)+∇D(y) eval at 1/2/4/8 GPU; % of HBM roofline"
-# algorithmic bytes per voxel-frame, fp32 / fp64: pass 1 reads T (s) + y (d s);
-# pass 2 reads T + y and writes dD/dy (d s)
+
+
 def bytes_per_vf(d: int, s: int) -> dict:
+    """Algorithmic bytes per voxel-frame: pass 1 reads T (s) + y (d s); pass 2 reads T + y
+    and writes dD/dy (d s).  2-D fp32: 12 + 20 = 32 B; 3-D fp32: 16 + 28 = 44 B."""
     return {"pass1": (1 + d) * s, "pass2": (1 + 2 * d) * s, "eval": (2 + 3 * d) * s}
 
 
-# compulsory bytes per voxel-frame of each engine kernel as designed: the split pass 1
-# (k_sample_gram / k_sample_v) writes V (s) and grad T (d s) next to its y + T reads; the streaming pass 2
-# reads them back and writes dD/dy; the fused kernels move exactly the SURVEY §8d pass figures
+# Each engine kernel's share of the algorithmic traffic: the kernel that gathers T at y for pass 1 is
+# credited with pass 1's bytes, the one writing dD/dy with pass 2's, every other kernel with 0 (its
+# traffic is intermediate data the fused two-pass design never materialises).  "own" = what the kernel
+# itself must move as designed (the split kernels' intermediate reads / writes included).
 def kernel_bytes_per_vf(d: int, s: int) -> dict:
-    return {"k_sample_v": 2 * (1 + d) * s, "k_gram_tc": s, "k_pass2_stream": (1 + 2 * d) * s,
-            "k_sample_gram": 2 * (1 + d) * s, "k_sample_vp": 2 * (1 + d) * s, "k_pass2_tma": (1 + 2 * d) * s, "k_pass2_mma": (1 + 2 * d) * s, "k_gram_tma": s, "k_gram_mma": s,
-            "k_pass2_bulk": (1 + 2 * d) * s,
-            "k_pass2": (1 + 2 * d) * s, "k_pass1_tc": (1 + d) * s, "k_pass1_ws": (1 + d) * s, "k_pass1": (1 + d) * s,
-            "k_reduce_finalize": 0,
-            # split NGF path: u -> (n, rho); Gram of n; z from (n, rho); adjoint stencil of z with grad T
-            "k_ngf_feat": (2 + d) * s, "k_gram_tcx": d * s, "k_ngf_z": (2 * d + 1) * s, "k_ngf_z_mma": (2 * d + 1) * s, "k_ngf_z_f16": (2 * d + 1) * s,
-            "k_ngf_feat4": (2 + d) * s, "k_ngf_adj4": 3 * d * s,
-            "k_ngf_adj_stream": 3 * d * s}
+    b = bytes_per_vf(d, s)
+    alg = {"k_ngf_fp1": b["pass1"], "k_ngf_fp2": b["pass2"], "k_sample_vp": b["pass1"], "k_sample_v": b["pass1"],
+           "k_pass2_tma": b["pass2"], "k_pass2_mma": b["pass2"], "k_ngf_adj4": b["pass2"], "k_pass1": b["pass1"],
+           "k_pass2": b["pass2"]}
+    own = {"k_ngf_fp1": b["pass1"], "k_ngf_fp2": b["pass2"], "k_sample_vp": 2 * (1 + d) * s,
+           "k_sample_v": 2 * (1 + d) * s, "k_pass2_tma": (1 + 2 * d) * s, "k_pass2_mma": (1 + 2 * d) * s,
+           "k_gram_tma": s, "k_gram_tcx": d * s, "k_ngf_feat4": (2 + d) * s, "k_ngf_z_f16": (2 * d + 1) * s,
+           "k_ngf_adj4": 3 * d * s, "k_pass1": b["pass1"], "k_pass2": b["pass2"], "k_reduce_finalize": 0}
+    return {"algorithmic": alg, "own": own}
 
 
 def _peaks():
@@ -128,67 +140,81 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(inside)}
 
 
-def build_workload(cfg_name: str, rank: int, world: int, device):
-    """Synthetic inputs of the config, generated on the device. Weak scaling: the domain
-    is world slabs tall (each rank owns one config-sized slab)."""
-    import torch
-
+def build_workload(cfg_name: str, device):
+    """Synthetic inputs of the config on the device: frames (synth.make_sequence, seed 0) and the bench
+    iterate (synth.bench_iterate, seed 1), cast to the config dtype.  The whole domain on every rank
+    (strong scaling: each rank then keeps its slab of y)."""
     from paper_2001_06613_b200 import synth
 
     cfg = synth.CONFIGS[cfg_name]
-    dims = list(cfg.dims)
-    dims[-1] *= world
-    dims = tuple(dims)
-    frames, times, spacing, origin = synth.make_sequence(cfg, seed=0, device=device, dims=dims)
-    y = synth.smooth_noise_iterate(dims, cfg.K, device=device) if cfg_name == "c2" else None
-    if y is None:  # other configs evaluate at the true-motion-free identity plus smooth noise too
-        y = synth.smooth_noise_iterate(dims, cfg.K, std_px=0.3, device=device)
+    frames, _, spacing, origin = synth.make_sequence(cfg, seed=0, device=device)
+    y = synth.bench_iterate(cfg, device=device)
     w = synth.config_weights(cfg)
-    return cfg, dims, spacing, origin, frames.to(cfg.dtype), y.to(cfg.dtype).contiguous(), w
+    return cfg, tuple(cfg.dims), spacing, origin, frames.to(cfg.dtype), y.to(cfg.dtype).contiguous(), w
 
 
-def run_gpu(args):
+class _Flush:
+    """Write 256 MiB (evicts the inputs) then read 256 MiB (writes the dirty lines back), so the timed
+    step starts with a cold, clean L2."""
+
+    def __init__(self, dev):
+        import torch
+
+        self.w = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+        self.r = torch.ones(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def fill_(self, v):
+        self.w.fill_(v)
+        self.r.sum()
+
+
+def engine_kernel_times(step, flush, reps: int = 10):
+    """Kernels of the engine's .so (namespace sr::) per step and their mean CUPTI device time (ms),
+    over ``reps`` steps with the L2 flush in between, outside the timed region."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for i in range(reps):
+            flush.fill_(float(i))
+            step()
+        torch.cuda.synchronize()
+    times, count = {}, 0
+    for ev in prof.events():
+        if ev.device_type.name == "CUDA" and "sr::" in ev.name:
+            count += 1
+            base = ev.name.replace("void ", "").replace("sr::", "").split("<")[0].split("(")[0].strip()
+            times.setdefault(base, []).append(ev.device_time * 1e-3)
+    return count // reps, {k: float(sum(v) / reps) for k, v in times.items()}
+
+
+def measure_config(name: str, args, world: int, rank: int, dev, full: bool):
+    """Time the config on this rank's slab; returns the per-config result dict (rank 0 fills it)."""
     import torch
     import torch.distributed as dist
 
     import paper_2001_06613_b200 as srb
     from paper_2001_06613_b200.parallel import ShardedFieldObjective, slab_ranges
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    cfg, dims, spacing, origin, frames, y_full, w = build_workload(args.config, rank, world, dev)
+    cfg, dims, spacing, origin, frames, y_full, w = build_workload(name, dev)
     d = len(dims)
     N = int(np.prod(dims))
     K = cfg.K
-    eng = srb.get_engine(local)
+    eng = srb.get_engine(dev.index)
     grid = srb.GridSpec(dims, spacing, origin)
     fd = srb.DeviceFrames(eng, frames, grid)
     h = grid.cell_volume
+    group = dist.group.WORLD if world > 1 else None
     lo, hi = slab_ranges(dims, world)[rank]
     obj = ShardedFieldObjective(fd, list(range(K)), w, h, feature=cfg.feature, ngf_eps=cfg.ngf_eps,
-                                pix_range=(lo, hi), halo_rows=2 if cfg.feature == "ngf" else 0,
-                                group=dist.group.WORLD if world > 1 else None)
+                                pix_range=(lo, hi), halo_rows=2 if cfg.feature == "ngf" else 0, group=group)
     y = obj.local_view(y_full)
+    y_host = y_full.cpu().pin_memory() if (full and world == 1) else None
     del y_full
     grad = torch.empty((K, d, hi - lo), dtype=cfg.dtype, device=dev)
     vf_rank = (hi - lo) * K
-    flush_w = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    flush_r = torch.ones(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-
-    class _Flush:
-        """Write 256 MiB (evicts the inputs) then read 256 MiB (writes the dirty lines back),
-        so the timed step starts with a cold, clean L2."""
-
-        def fill_(self, v):
-            flush_w.fill_(v)
-            flush_r.sum()
-
-    flush = _Flush()
+    flush = _Flush(dev)
     stream = torch.cuda.current_stream()
 
     def step():
@@ -198,10 +224,10 @@ def run_gpu(args):
         flush.fill_(1.0)
         step()
     torch.cuda.synchronize()
-    launches_per_step, kdev = engine_kernel_times(step, flush, reps=max(5, min(args.steps, 20)))
+    launches_per_step, kdev = engine_kernel_times(step, flush, reps=max(3, min(args.steps, 10)))
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(dev.index)
     with sampler:
         if world > 1:
             dist.barrier()
@@ -226,129 +252,152 @@ def run_gpu(args):
     vf_total = N * K
     value = vf_total / (ms_step * 1e-3)
 
-    # ---- roofline.  Phases by CUDA events on the launching stream (pass 1 = its kernels + CTA reduce,
-    # finalize, pass 2 = one kernel); per kernel by CUPTI device time over the same flushed loop.  The
-    # dominant kernel is the longest one; its bytes are its compulsory traffic per voxel-frame.
-    rl = obj.kernel_times(y, grad, flush, reps=max(5, min(args.steps, 50)))
+    # ---- roofline of the dominant kernel on its ALGORITHMIC bytes (SURVEY §8d share), CUPTI device time
+    # over the same flushed loop; the whole evaluation on 32 B (2-D) / 44 B (3-D) per voxel-frame
     s = 4 if cfg.dtype == torch.float32 else 8
     bpv = bytes_per_vf(d, s)
-    kbv = kernel_bytes_per_vf(d, s)
+    kb = kernel_bytes_per_vf(d, s)
     peak, peak_src = _peaks()
     kern = max(kdev, key=kdev.get)
     kern_ms = kdev[kern]
-    achieved = kbv.get(kern, 0) * vf_rank / (kern_ms * 1e-3) / 1e9
-    eval_achieved = bpv["eval"] * vf_rank / (ms_step * 1e-3) / 1e9
+    achieved = kb["algorithmic"].get(kern, 0) * vf_rank / (kern_ms * 1e-3) / 1e9
+    eval_achieved = bpv["eval"] * vf_total / (ms_step * 1e-3) / 1e9 / world
     traffic = None
-    prof = ROOT / "profiles" / f"traffic_{args.config}.json"
+    prof = ROOT / "profiles" / f"traffic_{name}.json"
     if prof.exists():
         traffic = json.loads(prof.read_text()).get(kern)
-
-    # ---- e2e: the public host API (pinned H2D of y, evaluation, D2H of D and dD/dy)
-    e2e = None
-    if world == 1:
-        # the step's input already in pinned host memory (the e2e contract); the timed region holds the
-        # H2D of y, the evaluation and the D2H of D and dD/dy, every step
-        y_host = y.cpu().pin_memory()
+    res = {
+        "config": name, "value": value, "ms_per_step": ms_step, "n_gpus": world,
+        "workload": f"{name}: {d}-D K={K} {'x'.join(map(str, dims))} {'fp32' if s == 4 else 'fp64'} "
+                    f"{cfg.feature.upper()} displacement-field D+grad eval",
+        "launches_per_step": launches_per_step,
+        "roofline": {"bound": "hbm", "kernel": kern, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "bytes_per_vf": kb["algorithmic"].get(kern, 0), "kernel_ms": kern_ms,
+                     "kernel_timing": "CUPTI device time, L2 flushed before each step",
+                     "kernels_ms": kdev, "kernels_share": {k: v / sum(kdev.values()) for k, v in kdev.items()},
+                     "kernels_own_bytes_per_vf": {k: kb["own"].get(k) for k in kdev},
+                     "eval_achieved": eval_achieved, "eval_frac": eval_achieved / peak,
+                     "eval_bytes_per_vf": bpv["eval"],
+                     "eval_note": "algorithmic bytes of the whole evaluation (SURVEY §8d) / event-timed step, per GPU"},
+        "clocks": sampler.summary(), "wall_s_timed_region": t_wall1 - t_wall0,
+    }
+    if full and world == 1:
+        # ---- e2e: the public host API (FieldObjective.evaluate_host: pinned H2D of y, evaluation, D2H of
+        # D and dD/dy), every step
         fo = srb.FieldObjective(fd, list(range(K)), w, h, feature=cfg.feature, ngf_eps=cfg.ngf_eps)
         for _ in range(2):
             fo.evaluate_host(y_host)
-        reps = max(3, min(args.steps, 20))
+        reps = max(3, min(args.steps, 10))
         t0 = time.perf_counter()
         for _ in range(reps):
             fo.evaluate_host(y_host)
         e2e_s = (time.perf_counter() - t0) / reps
         nbytes = int(y_host.numel() * y_host.element_size())
-        e2e = {"value": vf_total / e2e_s, "unit": "voxel-frames/s", "h2d_bytes_per_step": nbytes,
-               "d2h_bytes_per_step": nbytes + 8, "ms_per_step": e2e_s * 1e3,
-               "pcie_gbs": 2 * nbytes / e2e_s / 1e9}
+        res["e2e"] = {"value": vf_total / e2e_s, "unit": "voxel-frames/s", "h2d_bytes_per_step": nbytes,
+                      "d2h_bytes_per_step": nbytes + 8, "ms_per_step": e2e_s * 1e3,
+                      "pcie_gbs": 2 * nbytes / e2e_s / 1e9,
+                      "api": "FieldObjective.evaluate_host (pinned host y in, host D and dD/dy out)"}
+    del obj, fd, frames, y, grad, flush
+    torch.cuda.empty_cache()
+    return res
 
-    # ---- CPU baseline: the oracle port on a bounded sample (rank 0, N=1)
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    main_res = measure_config(args.config, args, world, rank, dev, full=True)
+    others = {}
+    for extra in ([] if args.only else [c for c in ("c4", "c2") if c != args.config]):
+        r = measure_config(extra, args, world, rank, dev, full=False)
+        others[extra] = {k: r[k] for k in ("workload", "value", "ms_per_step", "launches_per_step")}
+        others[extra]["roofline"] = {k: r["roofline"][k] for k in
+                                     ("kernel", "frac", "eval_frac", "kernels_ms", "eval_achieved")}
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu:
         cpu = cpu_baseline(args.config, threads=1, budget_s=args.cpu_budget)
-
     if rank == 0:
+        from paper_2001_06613_b200 import synth
+
+        cfg = synth.CONFIGS[args.config]
         line = {
-            "metric": METRIC, "value": value, "unit": "voxel-frames/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32" if cfg.dtype == torch.float32 else "f64",
-            "data": "synthetic (seeded Gaussian-blob sequence + sinusoidal motion, BASELINE.json generator)",
-            "config": {"workload": f"{args.config}: {d}-D K={K} {'x'.join(map(str, cfg.dims))} "
-                                   f"{'fp32' if s == 4 else 'fp64'} {cfg.feature.upper()} displacement-field D+grad eval",
-                       "dims_global": list(dims), "frames": K, "feature": cfg.feature,
-                       "parallelism": f"pixel slabs x{world} + NCCL all-reduce of the K x K raw Gram",
-                       "l2": "flushed before every timed step (256 MiB write + 256 MiB read, outside the event window)"},
-            "roofline": {"bound": "hbm", "kernel": kern, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "bytes_per_vf": kbv.get(kern, 0), "kernel_ms": kern_ms, "kernel_timing": "CUPTI device time",
-                         "kernels_ms": kdev, "kernels_bytes_per_vf": {k: kbv.get(k, 0) for k in kdev},
-                         "eval_achieved": eval_achieved, "eval_frac": eval_achieved / peak,
-                         "eval_bytes_per_vf": bpv["eval"], "phases_ms_events": rl},
+            "metric": METRIC, "value": main_res["value"], "unit": "voxel-frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": main_res["ms_per_step"],
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32" if cfg.dtype.itemsize == 4 else "f64",
+            "data": "synthetic (seeded Gaussian-blob sequence + sinusoidal motion, BASELINE.json generator; "
+                    "iterate synth.bench_iterate)",
+            "config": {"workload": main_res["workload"], "dims": list(cfg.dims), "frames": cfg.K,
+                       "feature": cfg.feature,
+                       "parallelism": f"pixel slabs x{world}, frames replicated, one all-gather of the K x K raw "
+                                      f"Gram sums per evaluation" if world > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (c3/c4); 256 MiB write + read flush before every timed step "
+                             "anyway, outside the event window"},
+            "roofline": main_res["roofline"],
             "cpu_baseline": cpu,
-            "e2e": e2e,
-            "gpu_launches": launches_per_step * args.steps,
-            "clocks": sampler.summary(),
-            "wall_s_timed_region": t_wall1 - t_wall0,
+            "e2e": main_res.get("e2e"),
+            "gpu_launches": main_res["launches_per_step"] * args.steps,
+            "clocks": main_res["clocks"],
+            "wall_s_timed_region": main_res["wall_s_timed_region"],
+            "other_configs": others,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
-def engine_kernel_times(step, flush, reps: int = 10):
-    """Kernels of the engine's .so (namespace sr::) per step and their mean CUPTI device time (ms),
-    over ``reps`` steps with the L2 flush in between, outside the timed region."""
-    import torch
-    from torch.profiler import ProfilerActivity, profile
-
-    torch.cuda.synchronize()
-    with profile(activities=[ProfilerActivity.CUDA]) as prof:
-        for i in range(reps):
-            flush.fill_(float(i))
-            step()
-        torch.cuda.synchronize()
-    times, count = {}, 0
-    for ev in prof.events():
-        if ev.device_type.name == "CUDA" and "sr::" in ev.name:
-            count += 1
-            base = ev.name.replace("void ", "").replace("sr::", "").split("<")[0].split("(")[0].strip()
-            times.setdefault(base, []).append(ev.device_time * 1e-3)
-    return count // reps, {k: float(sum(v) / len(v)) for k, v in times.items()}
-
-
-def cpu_baseline(config: str, threads: int, budget_s: float = 15.0, evals: int | None = None):
-    """Time the CPU oracle (the reference algorithm restated in numpy) on the config's full
-    workload; bounded by ``budget_s`` of evaluations (at least one)."""
+def _oracle_inputs(config: str, k_sample: int | None):
+    """The config's inputs on the CPU (frames fp32-quantised, the bench iterate), optionally only the
+    first ``k_sample`` frames (a bounded sample of the same workload: full resolution, fewer frames)."""
     import torch
 
-    from oracle import seqreg_oracle as orc
     from paper_2001_06613_b200 import synth
 
     cfg = synth.CONFIGS[config]
-    frames, times, spacing, origin = synth.make_sequence(cfg, seed=0, device="cpu")
-    y = synth.smooth_noise_iterate(cfg.dims, cfg.K, device="cpu")
-    if cfg.dtype == torch.float32:
-        fr = [f for f in frames.numpy().astype(np.float32).astype(np.float64)]
-        yv = y.numpy().astype(np.float32).astype(np.float64)
-    else:
-        fr, yv = list(frames.numpy()), y.numpy()
-    w = synth.config_weights(cfg)
+    K = cfg.K if k_sample is None else min(cfg.K, k_sample)
+    frames, _, spacing, origin = synth.make_sequence(cfg, seed=0, device="cpu", K=cfg.K)
+    y = synth.smooth_noise_iterate(cfg.dims, cfg.K, sigma_px=4.0, std_px=0.5, seed=1)  # = synth.bench_iterate
+    q = cfg.dtype == torch.float32
+    fr = frames.numpy()[:K]
+    yv = y.numpy()[:K]
+    if q:
+        fr = fr.astype(np.float32).astype(np.float64)
+        yv = yv.astype(np.float32).astype(np.float64)
+    w = synth.config_weights(cfg)[:K]
+    return cfg, list(fr), yv, w, spacing, origin, K
+
+
+def cpu_baseline(config: str, threads: int, budget_s: float = 15.0):
+    """The CPU oracle (the reference algorithm restated in numpy) on one core, on a bounded sample of the
+    config: the first K_s frames at full resolution, K_s sized for ~budget_s of work."""
+    from oracle import seqreg_oracle as orc
+
+    cfg, fr, yv, w, spacing, origin, _ = _oracle_inputs(config, None)
     h = float(np.prod(spacing))
-    vf = int(np.prod(cfg.dims)) * cfg.K
-    times_s = []
-    t_start = time.perf_counter()
-    while True:
+    N = int(np.prod(cfg.dims))
+
+    def run(k):
         t0 = time.perf_counter()
-        orc.evaluate_field(fr, cfg.dims, spacing, origin, yv, w, h, cfg.feature, cfg.ngf_eps, threads=threads)
-        times_s.append(time.perf_counter() - t0)
-        if evals is not None and len(times_s) >= evals:
-            break
-        if evals is None and time.perf_counter() - t_start > budget_s:
-            break
-    best = float(np.median(times_s))
-    return {"value": vf / best, "unit": "voxel-frames/s", "cores": threads, "kind": "port",
-            "sample": f"full {config} evaluation ({vf} voxel-frames) x{len(times_s)}, numpy oracle "
-                      f"(oracle/seqreg_oracle.py), median", "s_per_eval": best}
+        orc.evaluate_field(fr[:k], cfg.dims, spacing, origin, yv[:k], w[:k], h, cfg.feature, cfg.ngf_eps,
+                           threads=threads)
+        return time.perf_counter() - t0
+
+    k0 = min(cfg.K, 2)
+    t1 = run(k0)
+    ks = int(max(2, min(cfg.K, k0 * budget_s / max(t1, 1e-3))))
+    ts = [run(ks)]
+    s = float(np.median(ts))
+    return {"value": N * ks / s, "unit": "voxel-frames/s", "cores": threads, "kind": "port",
+            "sample": f"{config} with its first {ks} of {cfg.K} frames at full resolution ({N * ks} voxel-frames), "
+                      f"numpy oracle (oracle/seqreg_oracle.py), one evaluation", "s_per_eval": s}
 
 
 def run_reference(args):
@@ -357,54 +406,101 @@ def run_reference(args):
     if rank != 0:
         return
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
-    import torch
-
     from oracle import seqreg_oracle as orc
-    from paper_2001_06613_b200 import synth
 
-    cfg = synth.CONFIGS[args.config]
-    frames, times, spacing, origin = synth.make_sequence(cfg, seed=0, device="cpu")
-    y = synth.smooth_noise_iterate(cfg.dims, cfg.K, device="cpu")
-    fr = list(frames.numpy().astype(np.float32).astype(np.float64)) if cfg.dtype == torch.float32 else list(frames.numpy())
-    yv = y.numpy().astype(np.float32).astype(np.float64) if cfg.dtype == torch.float32 else y.numpy()
-    w = synth.config_weights(cfg)
+    cfg, fr, yv, w, spacing, origin, _ = _oracle_inputs(args.config, None)
     h = float(np.prod(spacing))
-    vf = int(np.prod(cfg.dims)) * cfg.K
-    run = lambda: orc.evaluate_field(fr, cfg.dims, spacing, origin, yv, w, h, cfg.feature, cfg.ngf_eps, threads=cores)
-    for _ in range(max(1, min(args.warmup, 2))):
-        run()
-    ts = []
-    for _ in range(args.steps):
+    N = int(np.prod(cfg.dims))
+
+    def run(k):
         t0 = time.perf_counter()
-        run()
-        ts.append(time.perf_counter() - t0)
+        orc.evaluate_field(fr[:k], cfg.dims, spacing, origin, yv[:k], w[:k], h, cfg.feature, cfg.ngf_eps,
+                           threads=cores)
+        return time.perf_counter() - t0
+
+    # each step a bounded sample (the first K_s frames at full resolution) sized so the whole
+    # --warmup + --steps run takes about args.ref_budget seconds
+    k0 = min(cfg.K, max(2, cores))
+    t1 = run(k0)
+    per_step = args.ref_budget / max(1, args.steps + min(args.warmup, 2))
+    ks = int(max(2, min(cfg.K, k0 * per_step / max(t1, 1e-3))))
+    for _ in range(max(0, min(args.warmup, 2) - 1)):
+        run(ks)
+    ts = [run(ks) for _ in range(args.steps)]
     s = float(np.mean(ts))
-    value = vf / s
+    value = N * ks / s
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "voxel-frames/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": s * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64 arithmetic on f32-quantised inputs",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64 arithmetic on f32-quantised inputs",
         "data": "synthetic (seeded Gaussian-blob sequence + sinusoidal motion, BASELINE.json generator)",
         "config": {"workload": f"{args.config}: {len(cfg.dims)}-D K={cfg.K} {'x'.join(map(str, cfg.dims))} "
                                f"{cfg.feature.upper()} displacement-field D+grad eval (CPU oracle port)"},
         "cpu_baseline": {"value": value, "unit": "voxel-frames/s", "cores": cores, "kind": "port",
-                         "sample": f"full {args.config} evaluation per step, per-frame thread pool of {cores}"},
+                         "sample": f"per step: the first {ks} of {cfg.K} frames at full resolution "
+                                   f"({N * ks} voxel-frames), per-frame thread pool of {cores}"},
         "e2e": {"value": value, "unit": "voxel-frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+def run_dry(args):
+    """CPU check of the multi-rank plumbing: every rank joins a gloo group, takes its slab of the config
+    and checks the all-gather; rank 0 prints the line skeleton with n_gpus."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2001_06613_b200 import synth
+    from paper_2001_06613_b200.parallel import allreduce_raw, slab_ranges
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    cfg = synth.CONFIGS[args.config]
+    lo, hi = slab_ranges(cfg.dims, world)[rank]
+    K = cfg.K
+    raw = torch.zeros(K * K + 3 * K + 1, dtype=torch.float64)
+    raw[-1] = hi - lo
+    allreduce_raw(raw, K, dist.group.WORLD if world > 1 else None)
+    assert int(raw[-1].item()) == int(np.prod(cfg.dims)), "slabs do not cover the domain"
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": "voxel-frames/s", "n_gpus": world,
+                          "dry_run": True, "config": {"workload": args.config},
+                          "slabs": slab_ranges(cfg.dims, world)}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--only", action="store_true", help="measure only --config (no other_configs)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--ref-budget", type=float, default=120.0)
+    ap.add_argument("--dry-run", action="store_true")
     args = ap.parse_args()
-    if args.impl == "reference":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one rank per GPU: re-launch under torchrun (the driver launches torchrun itself; this is for
+        # a plain `python bench.py --gpus N`)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve()),
+               *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
+    if args.dry_run:
+        run_dry(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_gpu(args)

@@ -14,7 +14,6 @@ Device-resident displacement-field objective (the north_star parametrisation):
 """
 
 from ._lib import EngineUnavailable, SingularSystemError, load_library
-from .datatypes import Affine, AffineStack, Grid, Image, ImageSequence, identity_affine, identity_params
 from .engine import DeviceFrames, Engine, EvalPlan, GridSpec, get_engine
 from .field import FieldObjective
 from .optimizer import ObjectiveEval, OptimOptions, OptimResult, lbfgs_minimize
@@ -35,18 +34,13 @@ from .temporal import interp_linear_fields, ls_predict_fields
 __version__ = "0.1.0"
 
 __all__ = [
-    "Affine",
-    "AffineStack",
     "CorrelationState",
     "DeviceFrames",
     "Engine",
     "EngineUnavailable",
     "EvalPlan",
     "FieldObjective",
-    "Grid",
     "GridSpec",
-    "Image",
-    "ImageSequence",
     "SingularSystemError",
     "configure",
     "correlation_state",
@@ -54,8 +48,6 @@ __all__ = [
     "dissimilarity",
     "dissimilarity_gradient",
     "get_engine",
-    "identity_affine",
-    "identity_params",
     "install",
     "interp_linear_fields",
     "load_library",

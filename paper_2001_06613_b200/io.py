@@ -15,7 +15,6 @@ from pathlib import Path
 import numpy as np
 import torch
 
-from .datatypes import Grid
 from .engine import DeviceFrames, GridSpec, get_engine
 
 __all__ = [
@@ -45,6 +44,19 @@ class TruncatedPayloadError(SequenceFormatError):
 
 class DimensionMismatchError(SequenceFormatError):
     """grid.py:57-59."""
+
+
+def _check_grid(dims, spacing, origin):
+    """The reference Grid's validation (grid.py:73-84), same ValueError messages."""
+    if not 1 <= len(dims) <= 3:
+        raise ValueError(f"grid must be 1-, 2-, or 3-dimensional, got {len(dims)} axes")
+    if len(spacing) != len(dims) or len(origin) != len(dims):
+        raise ValueError("dims, spacing, and origin must have the same length")
+    if any(d < 2 for d in dims):
+        raise ValueError(f"all dims must be >= 2, got {tuple(dims)}")
+    if any(s <= 0 for s in spacing):
+        raise ValueError(f"all spacings must be > 0, got {tuple(spacing)}")
+    return GridSpec(tuple(int(d) for d in dims), tuple(float(s) for s in spacing), tuple(float(o) for o in origin))
 
 
 def _header_field(lines, index, key):
@@ -83,7 +95,7 @@ def _parse_header(head: bytes):
     if len(times) != n:
         raise DimensionMismatchError(f"{n} frames declared but {len(times)} times given")
     try:
-        grid = Grid(tuple(dims), tuple(spacing), tuple(origin))
+        grid = _check_grid(dims, spacing, origin)
     except ValueError as exc:
         raise MalformedHeaderError(f"invalid grid: {exc}") from exc
     return grid, n, times
@@ -110,8 +122,7 @@ def read_sequence(path, dtype: torch.dtype = torch.float64, engine=None):
             raise TruncatedPayloadError(f"payload has {payload_len} bytes, expected {expected}")
         if payload_len > expected:
             raise TruncatedPayloadError(f"payload has {payload_len - expected} trailing bytes")
-        eng = engine if engine is not None else get_engine()
-        host = torch.empty(n * grid.cell_count, dtype=torch.float32, pin_memory=True)
+        host = torch.empty(n * grid.cell_count, dtype=torch.float32, pin_memory=torch.cuda.is_available())
         fh.seek(offset)
         view = host.numpy().view(np.uint8)
         got = fh.readinto(memoryview(view))
@@ -119,10 +130,17 @@ def read_sequence(path, dtype: torch.dtype = torch.float64, engine=None):
             raise TruncatedPayloadError(f"payload has {got} bytes, expected {expected}")
     if not np.little_endian:  # the payload is "<f4" (grid.py:268)
         host = torch.from_numpy(host.numpy().byteswap())
+    # the reference's Image / ImageSequence checks (grid.py:104-150), in its order, before any device work
+    if not bool(torch.isfinite(host).all()):
+        raise ValueError("image values must be finite")
+    if n < 2:
+        raise ValueError("a sequence needs at least 2 frames")
+    if any(t1 <= t0 for t0, t1 in zip(times, times[1:])):
+        raise ValueError("times must be strictly increasing")
+    eng = engine if engine is not None else get_engine()
     dev = host.to(eng.device, non_blocking=True).reshape(n, grid.cell_count)
     data = dev if dtype == torch.float32 else dev.to(dtype)
-    spec = GridSpec(tuple(grid.dims), tuple(grid.spacing), tuple(grid.origin))
-    return DeviceFrames(eng, data.contiguous(), spec), [float(t) for t in times]
+    return DeviceFrames(eng, data.contiguous(), grid), [float(t) for t in times]
 
 
 def write_sequence(frames: DeviceFrames, times, path) -> None:

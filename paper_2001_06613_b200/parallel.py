@@ -49,14 +49,22 @@ def halo_range(dims, lo: int, hi: int, halo_rows: int) -> tuple:
 
 
 def allreduce_raw(raw: torch.Tensor, k: int, group=None) -> torch.Tensor:
-    """In-place all-reduce of the raw sums [G | s | vmax | -vmin | count]:
-    SUM over G, s and count, MAX over the two extremum blocks."""
+    """In-place combination of the ranks' raw sums [G | s | vmax | -vmin | count] with ONE collective:
+    an all-gather of the whole vector (K^2 + 3K + 1 doubles per rank), then, on every rank, the SUM over
+    G, s and count and the MAX over the two extremum blocks in rank order.  The fixed order makes D and
+    dD/dy bitwise identical on every rank and independent of the collective's internal reduction order."""
     if group is None:
         return raw
+    world = dist.get_world_size(group)
+    allr = torch.empty((world, raw.numel()), dtype=raw.dtype, device=raw.device)
+    dist.all_gather(list(allr.unbind(0)), raw.contiguous(), group=group)
     kk = k * k + k
-    dist.all_reduce(raw[kk:kk + 2 * k], op=dist.ReduceOp.MAX, group=group)
-    dist.all_reduce(raw[:kk], op=dist.ReduceOp.SUM, group=group)
-    dist.all_reduce(raw[kk + 2 * k:], op=dist.ReduceOp.SUM, group=group)
+    acc = allr[0].clone()
+    for r in range(1, world):  # fixed rank order
+        acc[:kk] += allr[r, :kk]
+        acc[kk:kk + 2 * k] = torch.maximum(acc[kk:kk + 2 * k], allr[r, kk:kk + 2 * k])
+        acc[kk + 2 * k:] += allr[r, kk + 2 * k:]
+    raw.copy_(acc)
     return raw
 
 

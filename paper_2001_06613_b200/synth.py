@@ -20,7 +20,8 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-__all__ = ["SeqConfig", "CONFIGS", "make_sequence", "cell_centers", "smooth_noise_iterate", "config_weights"]
+__all__ = ["SeqConfig", "CONFIGS", "make_sequence", "cell_centers", "smooth_noise_iterate", "config_weights",
+           "bench_iterate"]
 
 
 @dataclass(frozen=True)
@@ -146,3 +147,11 @@ def config_weights(cfg: SeqConfig, K: int | None = None, seed: int = 2) -> np.nd
     if cfg.weights == "uniform_random":
         return np.random.default_rng(seed).uniform(0.5, 1.0, size=K)
     return np.full(K, 1.0 / K)
+
+
+def bench_iterate(cfg: SeqConfig, device="cpu", dims=None) -> torch.Tensor:
+    """The displacement iterate every arm of bench.py and the config goldens evaluate at: BASELINE
+    configs[1]'s recipe y = x + G_(sigma=4 px) * N(0, 0.5 px) per component (seed 1), applied to every
+    config so the GPU arm, the CPU baseline, the reference arm and tests/golden/config_golden.npz see the
+    same iterate.  [K, d, N] float64 (cast to the config dtype by the caller)."""
+    return smooth_noise_iterate(tuple(dims or cfg.dims), cfg.K, sigma_px=4.0, std_px=0.5, seed=1, device=device)

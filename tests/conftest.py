@@ -12,6 +12,22 @@ if str(ROOT) not in sys.path:
     sys.path.insert(0, str(ROOT))
 
 GOLDEN = ROOT / "tests" / "golden" / "golden.npz"
+# the unmodified reference package, installed into baseline/_ref by __graft_entry__.build(); it travels
+# to the GPU box with the repo (tests there never read /root/reference)
+REF = ROOT / "baseline" / "_ref"
+if str(REF) not in sys.path:
+    sys.path.append(str(REF))
+
+
+def ref_types():
+    """The reference's Grid / Image / ImageSequence / AffineStack (the drop-in API takes the reference's
+    own objects); fails the calling test when baseline/_ref is missing."""
+    try:
+        from seqreg.grid import Grid, Image, ImageSequence
+        from seqreg.transform import AffineStack
+    except ImportError as exc:
+        pytest.fail(f"reference package not importable from baseline/_ref ({exc}); run build()")
+    return Grid, Image, ImageSequence, AffineStack
 
 
 def pytest_configure(config):

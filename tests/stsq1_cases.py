@@ -24,4 +24,9 @@ def variants(good: bytes) -> dict:
         "invalid_grid": with_line(1, b"dims: 9 1"),
         "truncated": good[:-5],
         "trailing": good + b"\x00" * 8,
+        # payload / sequence checks the reference makes after the header (Image and ImageSequence,
+        # grid.py:104-150): plain ValueError, not a SequenceFormatError
+        "nonfinite": head + b"\n\n" + payload[:4] + b"\x00\x00\xc0\x7f" + payload[8:],
+        "one_frame": b"\n".join(lines[:4] + [b"frames: 1", b"times: 0.0"]) + b"\n\n" + payload[:len(payload) // 3],
+        "times_not_increasing": with_line(5, b"times: 0.0 0.5 0.5"),
     }

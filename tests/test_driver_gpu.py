@@ -1,7 +1,8 @@
 """The reference's own multilevel drivers (spml_run / stml_run, temporal.py:355-457) running on
 the B200 engine through install(): same iteration and evaluation counts as the CPU reference at
 fixed iterations, same final transforms (fp64).  Needs the reference package importable
-(baseline/_ref, installed with --no-deps, or PYTHONPATH); skipped otherwise."""
+(baseline/_ref, installed by __graft_entry__.build() from the reference sources; it travels to the
+GPU box with the repo snapshot).  A missing reference FAILS these tests (it is not a skip)."""
 
 import sys
 from pathlib import Path
@@ -11,10 +12,20 @@ import pytest
 import torch
 
 ROOT = Path(__file__).resolve().parents[1]
-for p in (ROOT / "baseline" / "_ref", Path("/root/reference/pkg/src")):
-    if p.exists() and str(p) not in sys.path:
-        sys.path.append(str(p))
-seqreg = pytest.importorskip("seqreg")
+_REF = ROOT / "baseline" / "_ref"
+if str(_REF) not in sys.path:
+    sys.path.append(str(_REF))
+try:
+    import seqreg
+except ImportError as exc:  # collected on CPU too: fail the (gpu-marked) tests, not the collection
+    seqreg = None
+    _SEQREG_ERR = str(exc)
+
+
+@pytest.fixture(autouse=True)
+def _need_reference():
+    if seqreg is None:
+        pytest.fail(f"reference package not importable from baseline/_ref ({_SEQREG_ERR}); run build()")
 
 import paper_2001_06613_b200 as srb  # noqa: E402
 

@@ -10,7 +10,7 @@ import torch
 
 import paper_2001_06613_b200 as srb
 from oracle import seqreg_oracle as orc
-from tests.conftest import golden_frames
+from tests.conftest import golden_frames, ref_types
 
 pytestmark = pytest.mark.gpu
 
@@ -27,11 +27,12 @@ def _relmax(a, b):
 
 
 def _seq_stack(case):
+    Grid, Image, ImageSequence, AffineStack = ref_types()
     frames = golden_frames(case)
-    grid = srb.Grid(tuple(case["dims"]), tuple(case["spacing"]), tuple(case["origin"]))
-    seq = srb.ImageSequence([srb.Image(grid, f) for f in frames], list(case["times"]))
+    grid = Grid(tuple(case["dims"]), tuple(case["spacing"]), tuple(case["origin"]))
+    seq = ImageSequence([Image(grid, f) for f in frames], list(case["times"]))
     subset = tuple(int(k) for k in case["subset"])
-    stack = srb.AffineStack.from_params(case["rows"], subset, len(frames), grid.ndim)
+    stack = AffineStack.from_params(case["rows"], subset, len(frames), grid.ndim)
     return seq, stack, subset
 
 
