@@ -392,7 +392,7 @@ static int corr_partial_impl(sr_ctx* c, const sr_problem* p, double* raw, double
     B.zstride = (B.zhi - B.zlo + 3) & ~3LL;
     const int d = g.nd;
     const size_t nv = (size_t)p->k * B.vstride, nz = (size_t)p->k * B.zstride;
-    const size_t total = nv * (1 + d) + nz * (2 * d + 1);  // u, grad T | n, z, rho
+    const size_t total = nv * (2 + d) + nz * (2 * d + 1);  // u, grad T, u lo | n, z, rho
     void* nb = c->ngfbuf;
     rc = ensure(&nb, &c->ngfbuf_bytes, total * 4);
     if (rc) return rc;
@@ -402,6 +402,7 @@ static int corr_partial_impl(sr_ctx* c, const sr_problem* p, double* raw, double
     B.Nf = B.G + nv * d;
     B.Z = B.Nf + nz * d;
     B.Rho = B.Z + nz * d;
+    B.VL = B.Rho + nz;
     c->vtag.valid = 0;
     const cudaError_t e1 = KP == 32 ? (d == 2 ? ngf_pass1_mma_d2(L, a, B, c->part, c->part_cap, &nblk)
                                               : ngf_pass1_mma_d3(L, a, B, c->part, c->part_cap, &nblk))

@@ -193,6 +193,75 @@ __device__ __forceinline__ T interp(const T* __restrict__ img, const Geo& g, con
 }
 
 
+// The value of the multilinear interpolant of an fp32 image in fp64 arithmetic (the corners are exact
+// fp32 numbers, the fractions exact in P): error ~1e-16 |u| instead of ~6e-8 |u|.  The NGF feature
+// takes central differences of u over one cell (h = 1/1024 at C3), which amplify an fp32 rounding of u
+// by 1/(2h) relative to grad u; with |grad u| ~ eps that exceeds the 1e-4 fp32 budget, so the NGF path
+// samples u through this and keeps it as an unevaluated fp32 pair hi + lo (hi = fl32(u), lo = fl32(u - hi)).
+// Same corner selection, hull test and zeroing as interp (grid.py:199-233).
+template <int D, bool POW2>
+__device__ __forceinline__ double interp_v64(const float* __restrict__ img, const Geo& g, const float (&p)[D],
+                                             float (&gr)[D]) {
+  bool inside = true;
+  float f[D];
+  int base = 0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    const float q = sub_rn(p[a], g.of[a]);
+    const float t = POW2 ? fmaf(q, g.invf[a], -0.5f) : sub_rn(div_rn(q, g.sf[a]), 0.5f);
+    const float hi = (float)(g.n[a] - 1);
+    const float tc = clampP(t, hi);
+    inside = inside && (tc == t);
+    const float fl = fminf(floorf(tc), hi - 1.f);
+    f[a] = tc - fl;
+    base += (int)fl * g.sti[a];
+  }
+  const float* q0 = img + base;
+  double val;
+  float gv[D];
+  if (D == 2) {
+    const int s1 = g.sti[1];
+    const float v00 = __ldg(q0), v10 = __ldg(q0 + 1), v01 = __ldg(q0 + s1), v11 = __ldg(q0 + s1 + 1);
+    const float d0 = v10 - v00, d1 = v11 - v01;
+    const float a0f = fmaf(f[0], d0, v00), a1f = fmaf(f[0], d1, v01);
+    gv[0] = fmaf(f[1], d1 - d0, d0);
+    gv[1] = a1f - a0f;
+    const double a0 = fma((double)f[0], (double)v10 - (double)v00, (double)v00);
+    const double a1 = fma((double)f[0], (double)v11 - (double)v01, (double)v01);
+    val = fma((double)f[1], a1 - a0, a0);
+  } else {
+    const int s1 = g.sti[1], s2 = g.sti[D == 3 ? 2 : 1];
+    float a[2][2], d[2][2];
+    double ad[2][2];
+#pragma unroll
+    for (int c2 = 0; c2 < 2; ++c2)
+#pragma unroll
+      for (int c1 = 0; c1 < 2; ++c1) {
+        const float* r = q0 + c1 * s1 + c2 * s2;
+        const float v0 = __ldg(r), v1 = __ldg(r + 1);
+        d[c1][c2] = v1 - v0;
+        a[c1][c2] = fmaf(f[0], d[c1][c2], v0);
+        ad[c1][c2] = fma((double)f[0], (double)v1 - (double)v0, (double)v0);
+      }
+    const float e0 = a[1][0] - a[0][0], e1 = a[1][1] - a[0][1];
+    const float b0 = fmaf(f[1], e0, a[0][0]), b1 = fmaf(f[1], e1, a[0][1]);
+    const float dz0 = fmaf(f[1], d[1][0] - d[0][0], d[0][0]);
+    const float dz1 = fmaf(f[1], d[1][1] - d[0][1], d[0][1]);
+    gv[0] = fmaf(f[2 % D], dz1 - dz0, dz0);
+    gv[1] = fmaf(f[2 % D], e1 - e0, e0);
+    gv[D - 1] = b1 - b0;
+    const double b0d = fma((double)f[1], ad[1][0] - ad[0][0], ad[0][0]);
+    const double b1d = fma((double)f[1], ad[1][1] - ad[0][1], ad[0][1]);
+    val = fma((double)f[D - 1], b1d - b0d, b0d);
+  }
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    const float gg = POW2 ? gv[a] * g.invf[a] : gv[a] / g.sf[a];
+    gr[a] = inside ? gg : 0.f;
+  }
+  return inside ? val : 0.0;
+}
+
 // ---- split multilinear sampling (2-D), used to batch the corner gathers of many samples:
 // prep: index + fractions + inside flag; fetch: the 4 corner loads; finish: the lerps.
 template <typename P, bool POW2>

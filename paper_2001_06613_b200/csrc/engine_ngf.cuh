@@ -51,8 +51,11 @@ __global__ void __launch_bounds__(256) k_ngf_feat(const Args a, const float* __r
 // The same arithmetic as k_ngf_feat (and ngf_at), 4 consecutive pixels per thread: one coordinate
 // decomposition per thread (then incremented), 32-bit offsets inside a frame's plane, 128-bit stores of
 // n and rho when the z plane allows them.  (k_ngf_feat: ~200 instructions per pixel, issue-bound.)
+// u = V + VL (an unevaluated fp32 pair, k_sample_vp<LO>): a difference of u is formed as
+// (V_+ - V_-) + (VL_+ - VL_-), accurate to fp32 relative to the difference itself.
 template <int D>
-__global__ void __launch_bounds__(256) k_ngf_feat4(const Args a, const float* __restrict__ V, long long vlo,
+__global__ void __launch_bounds__(256) k_ngf_feat4(const Args a, const float* __restrict__ V,
+                                                   const float* __restrict__ VL, long long vlo,
                                                    long long vstride, float* __restrict__ Nf, float* __restrict__ Rho,
                                                    long long zlo, long long zhi, long long zstride) {
   const int k = blockIdx.y;
@@ -60,6 +63,7 @@ __global__ void __launch_bounds__(256) k_ngf_feat4(const Args a, const float* __
   const int q0 = (blockIdx.x * 256 + threadIdx.x) * 4;  // z-relative first pixel
   if (q0 >= nz) return;
   const float* u = V + (long long)k * vstride + (zlo - vlo);  // u[q]: pixel zlo + q
+  const float* ul = VL + (long long)k * vstride + (zlo - vlo);
   float* nb = Nf + (long long)k * D * zstride;
   float* rb = Rho + (long long)k * zstride;
   const int p0 = (int)zlo + q0;
@@ -78,21 +82,26 @@ __global__ void __launch_bounds__(256) k_ngf_feat4(const Args a, const float* __
     float g4[D][4];
 #pragma unroll
     for (int ax = 0; ax < D; ++ax) {
-      float um[4], up[4];
+      float um[4], up[4], dl[4];
       if (ax == 0) {
         const float4 u0 = __ldg(reinterpret_cast<const float4*>(u + q0));
         um[0] = __ldg(u + q0 - 1), um[1] = u0.x, um[2] = u0.y, um[3] = u0.z;
         up[0] = u0.y, up[1] = u0.z, up[2] = u0.w, up[3] = __ldg(u + q0 + 4);
+        const float4 l0 = __ldg(reinterpret_cast<const float4*>(ul + q0));
+        dl[0] = l0.y - __ldg(ul + q0 - 1), dl[1] = l0.z - l0.x, dl[2] = l0.w - l0.y, dl[3] = __ldg(ul + q0 + 4) - l0.z;
       } else {
         const int st = a.g.sti[ax];
         const float4 m4 = __ldg(reinterpret_cast<const float4*>(u + q0 - st));
         const float4 p4 = __ldg(reinterpret_cast<const float4*>(u + q0 + st));
         um[0] = m4.x, um[1] = m4.y, um[2] = m4.z, um[3] = m4.w;
         up[0] = p4.x, up[1] = p4.y, up[2] = p4.z, up[3] = p4.w;
+        const float4 lm = __ldg(reinterpret_cast<const float4*>(ul + q0 - st));
+        const float4 lp = __ldg(reinterpret_cast<const float4*>(ul + q0 + st));
+        dl[0] = lp.x - lm.x, dl[1] = lp.y - lm.y, dl[2] = lp.z - lm.z, dl[3] = lp.w - lm.w;
       }
       const float inv = a.g.invf[ax];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) g4[ax][t] = (up[t] - um[t]) * (inv * 0.5f);
+      for (int t = 0; t < 4; ++t) g4[ax][t] = ((up[t] - um[t]) + dl[t]) * (inv * 0.5f);
     }
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
@@ -114,9 +123,10 @@ __global__ void __launch_bounds__(256) k_ngf_feat4(const Args a, const float* __
     for (int ax = 0; ax < D; ++ax) {
       const bool hp = c[ax] < a.g.n[ax] - 1, hm = c[ax] > 0;
       const int st = a.g.sti[ax];
-      const float up = __ldg(u + (hp ? q + st : q)), um = __ldg(u + (hm ? q - st : q));
+      const int qp = hp ? q + st : q, qm = hm ? q - st : q;
+      const float du = (__ldg(u + qp) - __ldg(u + qm)) + (__ldg(ul + qp) - __ldg(ul + qm));
       const float inv = a.g.invf[ax];
-      g[ax] = (hp && hm) ? (up - um) * (inv * 0.5f) : (up - um) * inv;
+      g[ax] = (hp && hm) ? du * (inv * 0.5f) : du * inv;
       pn += g[ax] * g[ax];
     }
     const float rho = sqrtf(pn + e * e);

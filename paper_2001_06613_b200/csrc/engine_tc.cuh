@@ -328,9 +328,10 @@ __global__ void __launch_bounds__(256, SPT <= 4 ? 8 : 4) k_sample_v(const Args a
 // k_sample_v with GV, software-pipelined over NI consecutive 1024-pixel blocks of one frame per CTA:
 // the y of block i + 1 is loaded before the gathers of block i, so only the gathers' latency is
 // exposed per block (k_sample_v exposes the y latency and then the gather latency).
-template <int D, bool POW2, int NI, int SPT = 4>
+// LO (NGF): u in fp64 arithmetic (interp_v64), written as V = fl32(u) and VL = fl32(u - V).
+template <int D, bool POW2, int NI, int SPT = 4, bool LO = false>
 __global__ void __launch_bounds__(256, 6) k_sample_vp(const Args a, float* __restrict__ V, float* __restrict__ G,
-                                                      long long vstride) {
+                                                      long long vstride, float* __restrict__ VL = nullptr) {
   constexpr int BP = 256 * SPT;
   const int npix = (int)(a.pix_hi - a.pix_lo);
   const int k = (int)blockIdx.y;
@@ -362,14 +363,23 @@ __global__ void __launch_bounds__(256, 6) k_sample_vp(const Args a, float* __res
     if (b0 >= npix) break;
     float pn[SPT][D];
     if (it + 1 < NI && b0 + BP < npix) load_y(blk + 1, pn);
-    float v[SPT], gd[SPT][D];
+    float v[SPT], vl[SPT], gd[SPT][D];
 #pragma unroll
-    for (int e = 0; e < SPT; ++e) v[e] = interp<float, float, D, true, POW2>(img, a.g, pc[e], gd[e]);
+    for (int e = 0; e < SPT; ++e) {
+      if (LO) {
+        const double u = interp_v64<D, POW2>(img, a.g, pc[e], gd[e]);
+        v[e] = (float)u;
+        vl[e] = (float)(u - (double)v[e]);
+      } else {
+        v[e] = interp<float, float, D, true, POW2>(img, a.g, pc[e], gd[e]);
+      }
+    }
     const int nb = npix - b0;
 #pragma unroll
     for (int e = 0; e < SPT; ++e) {
       const int pe = tid + 256 * e;
       if (pe < nb) {
+        if (LO) VL[(long long)k * vstride + b0 + pe] = vl[e];
         vk[b0 + pe] = v[e] - sh;
 #pragma unroll
         for (int c = 0; c < D; ++c) gk[(long long)c * vstride + b0 + pe] = gd[e][c];

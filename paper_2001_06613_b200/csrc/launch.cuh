@@ -288,11 +288,12 @@ cudaError_t run_pass1_split(const Launch& L, const Args& a, float* V, float* G, 
 // [zlo, zhi) = slab +- 1 row, the Gram over the slab.  cudaErrorNotSupported: layouts the TMA map cannot
 // express (the caller falls back to the generic kernels).
 // the split paths' sampling kernel launcher (mma_pass.cu)
-cudaError_t sample_vg_d2(const Launch& L, const Args& a, float* V, float* G, long long vstride);
-cudaError_t sample_vg_d3(const Launch& L, const Args& a, float* V, float* G, long long vstride);
+cudaError_t sample_vg_d2(const Launch& L, const Args& a, float* V, float* G, long long vstride, float* VL = nullptr);
+cudaError_t sample_vg_d3(const Launch& L, const Args& a, float* V, float* G, long long vstride, float* VL = nullptr);
 
 struct NgfBufs {
   float *V, *G, *Nf, *Rho, *Z;
+  float* VL;  // low fp32 parts of u (V + VL = u to ~1e-16 relative; interp_v64)
   long long vlo, vhi, vstride, zlo, zhi, zstride;
 };
 
@@ -321,10 +322,11 @@ cudaError_t run_ngf_pass1_kp(const Launch& L, const Args& a, const NgfBufs& B, d
   av.pix_lo = B.vlo;
   av.pix_hi = B.vhi;
   av.shifts = nullptr;
-  cudaError_t e = D == 2 ? sample_vg_d2(L, av, B.V, B.G, B.vstride) : sample_vg_d3(L, av, B.V, B.G, B.vstride);
+  cudaError_t e = D == 2 ? sample_vg_d2(L, av, B.V, B.G, B.vstride, B.VL)
+                         : sample_vg_d3(L, av, B.V, B.G, B.vstride, B.VL);
   if (e != cudaSuccess) return e;
   const dim3 fgrid((unsigned)((B.zhi - B.zlo + 1023) / 1024), (unsigned)a.K);
-  k_ngf_feat4<D><<<fgrid, 256, 0, L.stream>>>(a, B.V, B.vlo, B.vstride, B.Nf, B.Rho, B.zlo, B.zhi, B.zstride);
+  k_ngf_feat4<D><<<fgrid, 256, 0, L.stream>>>(a, B.V, B.VL, B.vlo, B.vstride, B.Nf, B.Rho, B.zlo, B.zhi, B.zstride);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const size_t smem = tgx_smem<KP>();

@@ -56,8 +56,16 @@ static int gram_sup() {
 // per CTA (33.0 vs 37.5 us at C2).  SEQREG_B200_SPT: 4 / 2 / 8 = k_sample_v with that many samples in
 // flight per thread, 44 = k_sample_vp over 4 blocks.
 template <int D>
-static cudaError_t launch_sample_vg(const Launch& L, const Args& a, float* V, float* G, long long vstride) {
+static cudaError_t launch_sample_vg(const Launch& L, const Args& a, float* V, float* G, long long vstride,
+                                    float* VL = nullptr) {
   const long long npix = a.pix_hi - a.pix_lo;
+  if (VL) {  // NGF: u as an fp32 pair (k_sample_vp<LO>)
+    const long long nblk = (npix + 1023) / 1024;
+    const dim3 sgrid((unsigned)((nblk + 1) / 2), (unsigned)a.K);
+    if (a.g.pow2) k_sample_vp<D, true, 2, 4, true><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride, VL);
+    else k_sample_vp<D, false, 2, 4, true><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride, VL);
+    return cudaGetLastError();
+  }
   // SEQREG_B200_SPT: samples in flight per thread of k_sample_v (2, 4 or 8)
   static const int spt = getenv("SEQREG_B200_SPT") ? atoi(getenv("SEQREG_B200_SPT")) : 42;
   if (spt == 8) {
@@ -96,11 +104,11 @@ static cudaError_t launch_sample_vg(const Launch& L, const Args& a, float* V, fl
   }
   return cudaGetLastError();
 }
-cudaError_t sample_vg_d2(const Launch& L, const Args& a, float* V, float* G, long long vstride) {
-  return launch_sample_vg<2>(L, a, V, G, vstride);
+cudaError_t sample_vg_d2(const Launch& L, const Args& a, float* V, float* G, long long vstride, float* VL) {
+  return launch_sample_vg<2>(L, a, V, G, vstride, VL);
 }
-cudaError_t sample_vg_d3(const Launch& L, const Args& a, float* V, float* G, long long vstride) {
-  return launch_sample_vg<3>(L, a, V, G, vstride);
+cudaError_t sample_vg_d3(const Launch& L, const Args& a, float* V, float* G, long long vstride, float* VL) {
+  return launch_sample_vg<3>(L, a, V, G, vstride, VL);
 }
 
 // 3-D view [rows][ncomp][npix] (row stride ncomp * stride, component stride `stride` floats) for the
@@ -148,10 +156,10 @@ static cudaError_t run_ngf_pass1_mma(const Launch& L, const Args& a, const NgfBu
   av.pix_lo = B.vlo;
   av.pix_hi = B.vhi;
   av.shifts = nullptr;
-  cudaError_t e = launch_sample_vg<D>(L, av, B.V, B.G, B.vstride);
+  cudaError_t e = launch_sample_vg<D>(L, av, B.V, B.G, B.vstride, B.VL);
   if (e != cudaSuccess) return e;
   const dim3 fgrid((unsigned)((B.zhi - B.zlo + 1023) / 1024), (unsigned)a.K);
-  k_ngf_feat4<D><<<fgrid, 256, 0, L.stream>>>(a, B.V, B.vlo, B.vstride, B.Nf, B.Rho, B.zlo, B.zhi, B.zstride);
+  k_ngf_feat4<D><<<fgrid, 256, 0, L.stream>>>(a, B.V, B.VL, B.vlo, B.vstride, B.Nf, B.Rho, B.zlo, B.zhi, B.zstride);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int sup = gram_sup();
