@@ -1191,150 +1191,6 @@ struct NZ {
   static constexpr int NT = 512, PW = 16, MW = D == 2 ? 4 : 2, NTL = 2 * D;  // n-tiles per item
 };
 
-template <int D>
-__global__ void __launch_bounds__(NZ<D>::NT, 1) k_ngf_z_mma(const Args a, const float* __restrict__ Nf,
-                                                           const float* __restrict__ Rho, long long zlo,
-                                                           long long zhi, long long zstride, float* __restrict__ Z) {
-  using C = NZ<D>;
-  constexpr int MW = C::MW, NTL = C::NTL, PW = C::PW;
-  extern __shared__ __align__(16) float4 nz_sh[];
-  const int K = a.K;
-  const int KS = (K + 7) / 8, JT = (K + 15) / 16;  // k-steps, m-tiles (frames padded with zeros)
-  float4* Ah = nz_sh;                // [JT][KS][32]
-  float4* Al = nz_sh + JT * KS * 32;  // lo
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = lane >> 2, t = lane & 3;
-  const StatsLayout L(K);
-  const double* Md = a.stats + L.M;
-  for (int e = tid; e < JT * KS * 32; e += C::NT) {
-    const int m = e / (KS * 32), ks = (e / 32) % KS, ln = e & 31;
-    const int gg = ln >> 2, tt = ln & 3;
-    float hv[4], lv[4];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {  // a0 (g, t), a1 (g + 8, t), a2 (g, t + 4), a3 (g + 8, t + 4); A[j][i] = M'[i][j]
-      const int j = 16 * m + gg + 8 * (r & 1), i = 8 * ks + tt + 4 * (r >> 1);
-      const double mv = (i < K && j < K) ? Md[i * K + j] : 0.0;
-      hv[r] = to_tf32((float)mv);
-      lv[r] = (float)(mv - (double)hv[r]);
-    }
-    Ah[e] = make_float4(hv[0], hv[1], hv[2], hv[3]);
-    Al[e] = make_float4(lv[0], lv[1], lv[2], lv[3]);
-  }
-  __syncthreads();
-  const int nzp = (int)(zhi - zlo);  // z range (32-bit: the launcher checks K D zstride < 2^31)
-  const int zs = (int)zstride;
-  const int nblk = (nzp + PW - 1) / PW;
-  const int ngrp = (JT + MW - 1) / MW;
-  const bool vec = (zs & 3) == 0 && ((reinterpret_cast<uintptr_t>(Nf) | reinterpret_cast<uintptr_t>(Rho) |
-                                     reinterpret_cast<uintptr_t>(Z)) & 15) == 0;
-  for (int item = blockIdx.x * (C::NT / 32) + warp; item < nblk * ngrp; item += gridDim.x * (C::NT / 32)) {
-    const int blk = item / ngrp, m0 = (item % ngrp) * MW;
-    const int mc = min(MW, JT - m0);
-    const int p0 = blk * PW;
-    const bool fullb = p0 + PW <= nzp && vec;
-    float acc[MW][NTL][4];
-#pragma unroll
-    for (int m = 0; m < MW; ++m)
-#pragma unroll
-      for (int nt = 0; nt < NTL; ++nt)
-#pragma unroll
-        for (int r = 0; r < 4; ++r) acc[m][nt][r] = 0.f;
-    // pixel of B column g in the n-tile pair half q
-    int pq[2];
-    bool okq[2];
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      pq[q] = p0 + 4 * (g >> 1) + 2 * q + (g & 1);
-      okq[q] = pq[q] < nzp;
-    }
-    for (int ks = 0; ks < KS; ++ks) {
-      uint32_t bh[NTL][2], bl[NTL][2];
-#pragma unroll
-      for (int nt = 0; nt < NTL; ++nt)
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int i = 8 * ks + t + 4 * u, c = nt >> 1, q = nt & 1;
-          const float v = (i < K && okq[q]) ? __ldg(Nf + ((i * D + c) * zs + pq[q])) : 0.f;
-          bh[nt][u] = __float_as_uint(v) & 0xffffe000u;  // hi by truncation, lo exact (see split_q)
-          bl[nt][u] = __float_as_uint(v - __uint_as_float(bh[nt][u]));
-        }
-#pragma unroll
-      for (int m = 0; m < MW; ++m) {
-        if (m < mc) {
-          const float4 ah = Ah[((m0 + m) * KS + ks) * 32 + lane], al = Al[((m0 + m) * KS + ks) * 32 + lane];
-          const uint32_t AH[4] = {__float_as_uint(ah.x), __float_as_uint(ah.y), __float_as_uint(ah.z),
-                                  __float_as_uint(ah.w)};
-          const uint32_t AL[4] = {__float_as_uint(al.x), __float_as_uint(al.y), __float_as_uint(al.z),
-                                  __float_as_uint(al.w)};
-          // one product at a time over the n-tiles: consecutive HMMAs hit independent accumulators
-#pragma unroll
-          for (int nt = 0; nt < NTL; ++nt) mma_tf32(acc[m][nt], AH, bh[nt][0], bh[nt][1]);
-#pragma unroll
-          for (int nt = 0; nt < NTL; ++nt) mma_tf32(acc[m][nt], AL, bh[nt][0], bh[nt][1]);
-#pragma unroll
-          for (int nt = 0; nt < NTL; ++nt) mma_tf32(acc[m][nt], AH, bl[nt][0], bl[nt][1]);
-        }
-      }
-    }
-    // epilogue: rows j = 16 (m0 + m) + g + 8 h, pixels p0 + 4t .. + 3
-    const int pz = p0 + 4 * t;
-#pragma unroll
-    for (int m = 0; m < MW; ++m)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int j = 16 * (m0 + m) + g + 8 * h;
-        if (m < mc && j < K) {
-          float r[D][4], n[D][4], rho[4];
-#pragma unroll
-          for (int c = 0; c < D; ++c) {
-            r[c][0] = acc[m][2 * c][2 * h];
-            r[c][1] = acc[m][2 * c][2 * h + 1];
-            r[c][2] = acc[m][2 * c + 1][2 * h];
-            r[c][3] = acc[m][2 * c + 1][2 * h + 1];
-          }
-          if (fullb) {
-#pragma unroll
-            for (int c = 0; c < D; ++c) {
-              const float4 v = __ldg(reinterpret_cast<const float4*>(Nf + ((j * D + c) * zs + pz)));
-              n[c][0] = v.x, n[c][1] = v.y, n[c][2] = v.z, n[c][3] = v.w;
-            }
-            const float4 v = __ldg(reinterpret_cast<const float4*>(Rho + (j * zs + pz)));
-            rho[0] = v.x, rho[1] = v.y, rho[2] = v.z, rho[3] = v.w;
-          } else {
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const bool ok = pz + u < nzp;
-#pragma unroll
-              for (int c = 0; c < D; ++c) n[c][u] = ok ? Nf[(j * D + c) * zs + pz + u] : 0.f;
-              rho[u] = ok ? Rho[j * zs + pz + u] : 1.f;
-            }
-          }
-          float zz[D][4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            float dot = 0.f;
-#pragma unroll
-            for (int c = 0; c < D; ++c) dot += n[c][u] * r[c][u];
-            const float ir = __frcp_rn(rho[u]);  // = 1.f / rho, correctly rounded, without the division sequence
-#pragma unroll
-            for (int c = 0; c < D; ++c) zz[c][u] = (r[c][u] - n[c][u] * dot) * ir;
-          }
-#pragma unroll
-          for (int c = 0; c < D; ++c) {
-            float* dst = Z + ((j * D + c) * zs + pz);
-            if (fullb) {
-              *reinterpret_cast<float4*>(dst) = make_float4(zz[c][0], zz[c][1], zz[c][2], zz[c][3]);
-            } else {
-#pragma unroll
-              for (int u = 0; u < 4; ++u)
-                if (pz + u < nzp) dst[u] = zz[c][u];
-            }
-          }
-        }
-      }
-  }
-}
-
 __device__ __forceinline__ void mma_f16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(
       "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
@@ -1352,7 +1208,7 @@ __device__ __forceinline__ void split_h2(float x0, float x1, uint32_t& hi, uint3
   lo = *reinterpret_cast<const uint32_t*>(&l);
 }
 
-// k_ngf_z_mma with f16 operands (default): the legacy tensor path runs m16n8k16 f16 at twice the
+// The K x K contraction of split NGF pass 2 for K <= 32 (k_ngf_z_tc above 32): the legacy tensor path runs m16n8k16 f16 at twice the
 // tf32 rate (scripts/probe_mma_sync.cu), so each product takes 3 f16 HMMAs per 16 frames instead of per 8.
 // 2-way split: x = hi + lo, hi = f16(x), lo = f16(x - hi): 22 significant bits, products exact in the
 // fp32 accumulator, a.b ~ hi hi + lo hi + hi lo.  n is in [-1, 1] (normalised gradients); M' is scaled by
@@ -1502,7 +1358,7 @@ __global__ void __launch_bounds__(NZ<D>::NT, 1) k_ngf_z_f16(const Args a, const 
             float dot = 0.f;
 #pragma unroll
             for (int c = 0; c < D; ++c) dot += n[c][u] * r[c][u];
-            const float ir = __frcp_rn(rho[u]);  // = 1.f / rho, correctly rounded, without the division sequence
+            const float ir = rho[u];  // IRho holds fl(1 / rho) (k_ngf_feat4)
 #pragma unroll
             for (int c = 0; c < D; ++c) zz[c][u] = (r[c][u] - n[c][u] * dot) * ir;
           }
@@ -1522,158 +1378,5 @@ __global__ void __launch_bounds__(NZ<D>::NT, 1) k_ngf_z_f16(const Args a, const 
   }
 }
 
-// k_ngf_z_f16 with 8-pixel items holding every m-tile (K <= 16 MT frames): each n value is loaded and
-// split once per item (the 16-pixel version loads it once per group of 4 m-tiles); B column g carries
-// pixel g of the item, so a lane's C fragments are pixels 2t, 2t + 1 (64-bit epilogue accesses).
-template <int D, int MT>
-__global__ void __launch_bounds__(512, 1) k_ngf_z_f16n(const Args a, const float* __restrict__ Nf,
-                                                      const float* __restrict__ Rho, long long zlo, long long zhi,
-                                                      long long zstride, float* __restrict__ Z) {
-  constexpr int NT = 512, PW = 8;
-  extern __shared__ __align__(16) uint4 nzn_sh[];
-  __shared__ float red_max[32];
-  const int K = a.K;
-  const int KS = (K + 15) / 16, JT = (K + 15) / 16;
-  uint4* Ah = nzn_sh;
-  uint4* Al = nzn_sh + JT * KS * 32;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = lane >> 2, t = lane & 3;
-  const StatsLayout L(K);
-  const double* Md = a.stats + L.M;
-  float mx = 0.f;
-  for (int e = tid; e < K * K; e += NT) mx = fmaxf(mx, fabsf((float)Md[e]));
-  mx = warp_max(mx);
-  if (lane == 0) red_max[warp] = mx;
-  __syncthreads();
-  if (warp == 0) {
-    float v = lane < NT / 32 ? red_max[lane] : 0.f;
-    v = warp_max(v);
-    if (lane == 0) red_max[0] = v;
-  }
-  __syncthreads();
-  const float mmax = red_max[0];
-  const int sexp = mmax > 0.f ? 13 - ilogbf(mmax) : 0;
-  const float scale = ldexpf(1.f, sexp), unscale = ldexpf(1.f, -sexp);
-  for (int e = tid; e < JT * KS * 32; e += NT) {
-    const int m = e / (KS * 32), ks = (e / 32) % KS, ln = e & 31;
-    const int gg = ln >> 2, tt = ln & 3;
-    uint32_t hv[4], lv[4];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int j = 16 * m + gg + 8 * (r & 1), i = 16 * ks + 2 * tt + 8 * (r >> 1);
-      const float m0 = (i < K && j < K) ? (float)Md[i * K + j] * scale : 0.f;
-      const float m1 = (i + 1 < K && j < K) ? (float)Md[(i + 1) * K + j] * scale : 0.f;
-      split_h2(m0, m1, hv[r], lv[r]);
-    }
-    Ah[e] = make_uint4(hv[0], hv[1], hv[2], hv[3]);
-    Al[e] = make_uint4(lv[0], lv[1], lv[2], lv[3]);
-  }
-  __syncthreads();
-  const int nzp = (int)(zhi - zlo);
-  const int zs = (int)zstride;
-  const int nblk = (nzp + PW - 1) / PW;
-  const bool vec = (zs & 1) == 0 && ((reinterpret_cast<uintptr_t>(Nf) | reinterpret_cast<uintptr_t>(Rho) |
-                                     reinterpret_cast<uintptr_t>(Z)) & 7) == 0;
-  for (int blk = blockIdx.x * (NT / 32) + warp; blk < nblk; blk += gridDim.x * (NT / 32)) {
-    const int p0 = blk * PW;
-    const bool fullb = p0 + PW <= nzp && vec;
-    float acc[MT][D][4];
-#pragma unroll
-    for (int m = 0; m < MT; ++m)
-#pragma unroll
-      for (int c = 0; c < D; ++c)
-#pragma unroll
-        for (int r = 0; r < 4; ++r) acc[m][c][r] = 0.f;
-    const int pg = p0 + g;
-    const bool okg = pg < nzp;
-    auto load_n = [&](int ks, float (&nv)[D][2][2]) {
-#pragma unroll
-      for (int c = 0; c < D; ++c)
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int i = 16 * ks + 2 * t + 8 * u;
-          nv[c][u][0] = (i < K && okg) ? __ldg(Nf + ((i * D + c) * zs + pg)) : 0.f;
-          nv[c][u][1] = (i + 1 < K && okg) ? __ldg(Nf + (((i + 1) * D + c) * zs + pg)) : 0.f;
-        }
-    };
-    float nvc[D][2][2];
-    load_n(0, nvc);
-    for (int ks = 0; ks < KS; ++ks) {
-      uint32_t bh[D][2], bl[D][2];
-#pragma unroll
-      for (int c = 0; c < D; ++c)
-#pragma unroll
-        for (int u = 0; u < 2; ++u) split_h2(nvc[c][u][0], nvc[c][u][1], bh[c][u], bl[c][u]);
-      if (ks + 1 < KS) load_n(ks + 1, nvc);
-#pragma unroll
-      for (int m = 0; m < MT; ++m) {
-        if (m < JT) {
-          const uint4 ah = Ah[(m * KS + ks) * 32 + lane], al = Al[(m * KS + ks) * 32 + lane];
-          const uint32_t AH[4] = {ah.x, ah.y, ah.z, ah.w}, AL[4] = {al.x, al.y, al.z, al.w};
-#pragma unroll
-          for (int c = 0; c < D; ++c) mma_f16(acc[m][c], AH, bh[c][0], bh[c][1]);
-#pragma unroll
-          for (int c = 0; c < D; ++c) mma_f16(acc[m][c], AL, bh[c][0], bh[c][1]);
-#pragma unroll
-          for (int c = 0; c < D; ++c) mma_f16(acc[m][c], AH, bl[c][0], bl[c][1]);
-        }
-      }
-    }
-    // epilogue: acc[m][c][2h + u] = r_(j, c)(p0 + 2t + u), j = 16 m + g + 8 h
-    const int pz = p0 + 2 * t;
-#pragma unroll
-    for (int m = 0; m < MT; ++m)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int j = 16 * m + g + 8 * h;
-        if (m < JT && j < K) {
-          float r[D][2], n[D][2], rho[2];
-#pragma unroll
-          for (int c = 0; c < D; ++c) {
-            r[c][0] = acc[m][c][2 * h] * unscale;
-            r[c][1] = acc[m][c][2 * h + 1] * unscale;
-          }
-          if (fullb) {
-#pragma unroll
-            for (int c = 0; c < D; ++c) {
-              const float2 v = __ldg(reinterpret_cast<const float2*>(Nf + ((j * D + c) * zs + pz)));
-              n[c][0] = v.x, n[c][1] = v.y;
-            }
-            const float2 v = __ldg(reinterpret_cast<const float2*>(Rho + (j * zs + pz)));
-            rho[0] = v.x, rho[1] = v.y;
-          } else {
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              const bool ok = pz + u < nzp;
-#pragma unroll
-              for (int c = 0; c < D; ++c) n[c][u] = ok ? Nf[(j * D + c) * zs + pz + u] : 0.f;
-              rho[u] = ok ? Rho[j * zs + pz + u] : 1.f;
-            }
-          }
-          float zz[D][2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            float dot = 0.f;
-#pragma unroll
-            for (int c = 0; c < D; ++c) dot += n[c][u] * r[c][u];
-            const float ir = __frcp_rn(rho[u]);
-#pragma unroll
-            for (int c = 0; c < D; ++c) zz[c][u] = (r[c][u] - n[c][u] * dot) * ir;
-          }
-#pragma unroll
-          for (int c = 0; c < D; ++c) {
-            float* dst = Z + ((j * D + c) * zs + pz);
-            if (fullb) {
-              *reinterpret_cast<float2*>(dst) = make_float2(zz[c][0], zz[c][1]);
-            } else {
-#pragma unroll
-              for (int u = 0; u < 2; ++u)
-                if (pz + u < nzp) dst[u] = zz[c][u];
-            }
-          }
-        }
-      }
-  }
-}
 
 }  // namespace sr

@@ -1,12 +1,14 @@
 // engine_ngf.cuh — split NGF path (fp32, displacement fields, K <= 128): no neighbour re-sampling,
 // tensor-core Gram, streaming pass 2.  DESIGN.md §4.
 //
-//   k_sample_v (engine_tc.cuh, no shift)  u = T_k(y_k) and grad T_k over the slab +- 2 rows
-//   k_ngf_feat                             n = grad_h u / rho, rho = sqrt(|grad_h u|^2 + eps^2)
+//   k_sample_vp<LO> (engine_tc.cuh)        u = T_k(y_k) (fp64 arithmetic, kept as an fp32 pair) and
+//                                          grad T_k over the slab +- 2 rows
+//   k_ngf_feat4                            n = grad_h u / rho, 1/rho, rho = sqrt(|grad_h u|^2 + eps^2)
 //                                          (the stencil of ngf_at, engine.cuh) over the slab +- 1 row
 //   k_gram_tcx<64|128>                     raw Gram  sum_(p, c) n_i n_j  over the slab on tcgen05 (3xTF32)
-//   k_ngf_z                                r = M'^T n (per pixel and component), z = (r - n (n.r)) / rho
-//   k_ngf_adj_stream                       dD/dy = (D_h^T z) grad T
+//   k_ngf_z_tc (engine_ngf_tc.cuh)         r = M'^T n (per pixel and component) on tcgen05,
+//                                          z = (r - n (n.r)) / rho
+//   k_ngf_adj4                             dD/dy = (D_h^T z) grad T
 #pragma once
 
 namespace sr {
@@ -17,38 +19,9 @@ __device__ __forceinline__ void coords_flat(const Geo& g, int p, int (&c)[3]) {
   c[2] = g.nd > 2 ? p / (g.n[0] * g.n[1]) : 0;
 }
 
-// n, rho at pixels [zlo, zhi) of every subset frame from u = V[k][p - vlo] (same float arithmetic
-// as ngf_at: central differences inside, one-sided at the domain edge, world units)
-template <int D>
-__global__ void __launch_bounds__(256) k_ngf_feat(const Args a, const float* __restrict__ V, long long vlo,
-                                                  long long vstride, float* __restrict__ Nf, float* __restrict__ Rho,
-                                                  long long zlo, long long zhi, long long zstride) {
-  const int k = blockIdx.y;
-  const long long p = zlo + (long long)blockIdx.x * 256 + threadIdx.x;
-  if (p >= zhi) return;
-  int c[3];
-  coords_flat(a.g, (int)p, c);
-  const float* u = V + (long long)k * vstride - vlo;
-  float g[D];
-  float pn = 0.f;
-#pragma unroll
-  for (int ax = 0; ax < D; ++ax) {
-    const bool hp = c[ax] < a.g.n[ax] - 1, hm = c[ax] > 0;
-    const long long st = a.g.sti[ax];
-    const float up = __ldg(u + (hp ? p + st : p)), um = __ldg(u + (hm ? p - st : p));
-    const float inv = (float)a.g.inv[ax];
-    g[ax] = (hp && hm) ? (up - um) * (inv * 0.5f) : (up - um) * inv;
-    pn += g[ax] * g[ax];
-  }
-  const float e = (float)a.eps;
-  const float rho = sqrtf(pn + e * e);
-  const float ir = 1.f / rho;
-#pragma unroll
-  for (int ax = 0; ax < D; ++ax) Nf[((long long)k * D + ax) * zstride + (p - zlo)] = g[ax] * ir;
-  Rho[(long long)k * zstride + (p - zlo)] = rho;
-}
-
-// The same arithmetic as k_ngf_feat (and ngf_at), 4 consecutive pixels per thread: one coordinate
+// n and 1/rho at pixels [zlo, zhi) of every subset frame (the stencil and float arithmetic of ngf_at,
+// engine.cuh: central differences inside, one-sided at the domain edge, world units), 4 consecutive pixels
+// per thread: one coordinate
 // decomposition per thread (then incremented), 32-bit offsets inside a frame's plane, 128-bit stores of
 // n and rho when the z plane allows them.  (k_ngf_feat: ~200 instructions per pixel, issue-bound.)
 // u = V + VL (an unevaluated fp32 pair, k_sample_vp<LO>): a difference of u is formed as
@@ -56,7 +29,7 @@ __global__ void __launch_bounds__(256) k_ngf_feat(const Args a, const float* __r
 template <int D>
 __global__ void __launch_bounds__(256) k_ngf_feat4(const Args a, const float* __restrict__ V,
                                                    const float* __restrict__ VL, long long vlo,
-                                                   long long vstride, float* __restrict__ Nf, float* __restrict__ Rho,
+                                                   long long vstride, float* __restrict__ Nf, float* __restrict__ IRho,
                                                    long long zlo, long long zhi, long long zstride) {
   const int k = blockIdx.y;
   const int nz = (int)(zhi - zlo);
@@ -65,7 +38,7 @@ __global__ void __launch_bounds__(256) k_ngf_feat4(const Args a, const float* __
   const float* u = V + (long long)k * vstride + (zlo - vlo);  // u[q]: pixel zlo + q
   const float* ul = VL + (long long)k * vstride + (zlo - vlo);
   float* nb = Nf + (long long)k * D * zstride;
-  float* rb = Rho + (long long)k * zstride;
+  float* rb = IRho + (long long)k * zstride;
   const int p0 = (int)zlo + q0;
   int c[3];
   coords_flat(a.g, p0, c);
@@ -112,7 +85,7 @@ __global__ void __launch_bounds__(256) k_ngf_feat4(const Args a, const float* __
       const float ir = 1.f / rho;
 #pragma unroll
       for (int ax = 0; ax < D; ++ax) nv[ax][t] = g4[ax][t] * ir;
-      rv[t] = rho;
+      rv[t] = ir;
     }
   } else
 #pragma unroll
@@ -133,7 +106,7 @@ __global__ void __launch_bounds__(256) k_ngf_feat4(const Args a, const float* __
     const float ir = __frcp_rn(rho);  // = 1.f / rho (correctly rounded)
 #pragma unroll
     for (int ax = 0; ax < D; ++ax) nv[ax][t] = g[ax] * ir;
-    rv[t] = rho;
+    rv[t] = ir;
     if (++c[0] == a.g.n[0]) {  // next pixel
       c[0] = 0;
       if (D > 1 && ++c[1] == a.g.n[1]) {
@@ -158,7 +131,7 @@ __global__ void __launch_bounds__(256) k_ngf_feat4(const Args a, const float* __
   }
 }
 
-// k_ngf_adj_stream with 4 consecutive pixels per thread (same arithmetic as dgrad_adjoint), 128-bit
+// dD/dy = (D_h^T z) grad T, 4 consecutive pixels per thread (same arithmetic as dgrad_adjoint), 128-bit
 // grad T loads and dD/dy stores when aligned.
 template <int D>
 __global__ void __launch_bounds__(256) k_ngf_adj4(const Args a, const float* __restrict__ Z, long long zlo,
@@ -446,101 +419,6 @@ __global__ void __launch_bounds__(TGX<KP>::NT, 1) k_gram_tcx(const Args a, const
     tc_fence_after();
     tmem_dealloc(tmem, NC * NA);
   }
-}
-
-// ------------------------------------------------------------------------------------------
-// z over [zlo, zhi): block = ZP pixels x G groups of 16 frames.  The block's n tile [K][D][ZP] is
-// staged in shared memory once (coalesced); thread (pixel, group) forms r_(j,c) = sum_i M'_ij n_(i,c)
-// for its 16 frames (M' broadcast from shared memory), then z_(j,c) = (r_(j,c) - n_(j,c)
-// sum_c' n_(j,c') r_(j,c')) / rho_j.
-constexpr int NGF_ZP = 32, NGF_JG = 16;
-
-template <int D>
-__global__ void __launch_bounds__(256) k_ngf_z(const Args a, const float* __restrict__ Nf,
-                                               const float* __restrict__ Rho, long long zlo, long long zhi,
-                                               long long zstride, float* __restrict__ Z) {
-  constexpr int ZP = NGF_ZP, JG = NGF_JG;
-  extern __shared__ __align__(16) float sm_ngfz[];
-  const int K = a.K;
-  const int KP16 = (K + JG - 1) / JG * JG;
-  float* Ms = sm_ngfz;                        // [K][KP16], zero padded
-  float* Ns = Ms + (size_t)K * KP16;          // [K][D][ZP]
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const StatsLayout L(K);
-  const float* Mg = coef_ptr<float>(a.stats, L);
-  for (int e = tid; e < K * KP16; e += nt) {
-    const int i = e / KP16, j = e % KP16;
-    Ms[e] = j < K ? Mg[i * K + j] : 0.f;
-  }
-  const long long p0 = zlo + (long long)blockIdx.x * ZP;
-  for (int e = tid; e < K * D * ZP; e += nt) {
-    const int ic = e / ZP, px = e % ZP;
-    const long long p = p0 + px;
-    Ns[e] = p < zhi ? __ldg(Nf + (long long)ic * zstride + (p - zlo)) : 0.f;
-  }
-  __syncthreads();
-  const int px = tid % ZP, grp = tid / ZP, j0 = grp * JG;
-  const long long p = p0 + px;
-  if (j0 >= K || p >= zhi) return;
-  float r[JG][D];
-#pragma unroll
-  for (int jj = 0; jj < JG; ++jj)
-#pragma unroll
-    for (int c = 0; c < D; ++c) r[jj][c] = 0.f;
-#pragma unroll 2
-  for (int i = 0; i < K; ++i) {
-    float ni[D];
-#pragma unroll
-    for (int c = 0; c < D; ++c) ni[c] = Ns[(i * D + c) * ZP + px];
-    const float4* m4 = reinterpret_cast<const float4*>(Ms + i * KP16 + j0);
-#pragma unroll
-    for (int q = 0; q < JG / 4; ++q) {
-      const float4 m = m4[q];
-      const float mm[4] = {m.x, m.y, m.z, m.w};
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int c = 0; c < D; ++c) r[4 * q + u][c] = fmaf(mm[u], ni[c], r[4 * q + u][c]);
-    }
-  }
-  const long long pz = p - zlo;
-#pragma unroll
-  for (int jj = 0; jj < JG; ++jj) {
-    const int j = j0 + jj;
-    if (j >= K) break;
-    float nj[D], dot = 0.f;
-#pragma unroll
-    for (int c = 0; c < D; ++c) {
-      nj[c] = Ns[(j * D + c) * ZP + px];
-      dot += nj[c] * r[jj][c];
-    }
-    const float ir = 1.f / __ldg(Rho + (long long)j * zstride + pz);
-#pragma unroll
-    for (int c = 0; c < D; ++c) Z[((long long)j * D + c) * zstride + pz] = (r[jj][c] - nj[c] * dot) * ir;
-  }
-}
-
-// dD/dy_(k,c)(p) = (sum_ax D_h,ax^T z_(k,ax))(p) grad T_(k,c)(p) over the slab
-template <int D>
-__global__ void __launch_bounds__(256) k_ngf_adj_stream(const Args a, const float* __restrict__ Z, long long zlo,
-                                                        long long zstride, const float* __restrict__ Gv,
-                                                        long long vlo, long long vstride) {
-  const int k = blockIdx.y;
-  const long long p = a.pix_lo + (long long)blockIdx.x * 256 + threadIdx.x;
-  if (p >= a.pix_hi) return;
-  int c[3];
-  coords_flat(a.g, (int)p, c);
-  float du = 0.f;
-#pragma unroll
-  for (int ax = 0; ax < D; ++ax) {
-    const float* z = Z + ((long long)k * D + ax) * zstride;
-    du += dgrad_adjoint<float, D>(z, p - zlo, a.g.st[ax], c[ax], a.g.n[ax], (float)a.g.inv[ax]);
-  }
-  float* out = reinterpret_cast<float*>(a.out);
-#pragma unroll
-  for (int cc = 0; cc < D; ++cc)
-    out[((long long)k * D + cc) * a.o_stride + (p - a.o_off)] =
-        du * __ldg(Gv + ((long long)k * D + cc) * vstride + (p - vlo));
 }
 
 }  // namespace sr

@@ -292,7 +292,7 @@ cudaError_t sample_vg_d2(const Launch& L, const Args& a, float* V, float* G, lon
 cudaError_t sample_vg_d3(const Launch& L, const Args& a, float* V, float* G, long long vstride, float* VL = nullptr);
 
 struct NgfBufs {
-  float *V, *G, *Nf, *Rho, *Z;
+  float *V, *G, *Nf, *Rho, *Z;  // Rho holds 1/rho (k_ngf_feat4)
   float* VL;  // low fp32 parts of u (V + VL = u to ~1e-16 relative; interp_v64)
   long long vlo, vhi, vstride, zlo, zhi, zstride;
 };
@@ -358,26 +358,9 @@ cudaError_t ngf_z_mma_d3(const Launch& L, const Args& a, const NgfBufs& B);
 
 template <int D>
 cudaError_t run_ngf_pass2(const Launch& L, const Args& a, const NgfBufs& B) {
-  const int K = a.K;
-  static const bool zmma = !(getenv("SEQREG_B200_NGFZ") && getenv("SEQREG_B200_NGFZ")[0] == '0');
-  cudaError_t ez = cudaErrorNotSupported;
-  if (zmma) ez = D == 2 ? ngf_z_mma_d2(L, a, B) : ngf_z_mma_d3(L, a, B);
-  if (ez == cudaSuccess) {
-    const dim3 g2((unsigned)((a.pix_hi - a.pix_lo + 1023) / 1024), (unsigned)K);
-    k_ngf_adj4<D><<<g2, 256, 0, L.stream>>>(a, B.Z, B.zlo, B.zstride, B.G, B.vlo, B.vstride);
-    return cudaGetLastError();
-  }
-  if (ez != cudaErrorNotSupported) return ez;
-  const int groups = (K + NGF_JG - 1) / NGF_JG;
-  const int KP16 = groups * NGF_JG;
-  const size_t smem = ((size_t)K * KP16 + (size_t)K * D * NGF_ZP) * 4;
-  cudaError_t e = cudaFuncSetAttribute(k_ngf_z<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  k_ngf_z<D><<<(unsigned)((B.zhi - B.zlo + NGF_ZP - 1) / NGF_ZP), NGF_ZP * groups, smem, L.stream>>>(
-      a, B.Nf, B.Rho, B.zlo, B.zhi, B.zstride, B.Z);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  const dim3 g2((unsigned)((a.pix_hi - a.pix_lo + 1023) / 1024), (unsigned)K);
+  const cudaError_t ez = D == 2 ? ngf_z_mma_d2(L, a, B) : ngf_z_mma_d3(L, a, B);
+  if (ez != cudaSuccess) return ez;
+  const dim3 g2((unsigned)((a.pix_hi - a.pix_lo + 1023) / 1024), (unsigned)a.K);
   k_ngf_adj4<D><<<g2, 256, 0, L.stream>>>(a, B.Z, B.zlo, B.zstride, B.G, B.vlo, B.vstride);
   return cudaGetLastError();
 }

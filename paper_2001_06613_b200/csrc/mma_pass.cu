@@ -3,6 +3,7 @@
 #include <cstdlib>
 #include <utility>
 #include "engine_mma.cuh"
+#include "engine_ngf_tc.cuh"
 #include "launch.cuh"
 
 namespace sr {
@@ -264,32 +265,17 @@ static cudaError_t run_pass2_mma(const Launch& L, const Args& a, const float* V,
   return launch_pdl(kern, dim3(grid), dim3(P2M::NT), 0, L.stream, a, V, G, vstride);
 }
 
+// Split NGF pass 2 contraction: k_ngf_z_tc (tcgen05 kind::f16, engine_ngf_tc.cuh), K <= 128
 template <int D>
 static cudaError_t run_ngf_z_mma(const Launch& L, const Args& a, const NgfBufs& B) {
-  using C = NZ<D>;
   const int K = a.K;
   const long long nzp = B.zhi - B.zlo;
   if (nzp <= 0) return cudaSuccess;
-  if ((long long)K * D * B.zstride >= (1LL << 31)) return cudaErrorNotSupported;
-  const int JT = (K + 15) / 16;
-  const long long items = (nzp + C::PW - 1) / C::PW * ((JT + C::MW - 1) / C::MW);
-  // SEQREG_B200_NGFZ=2: tf32 operands (k_ngf_z_mma); default f16 operands (k_ngf_z_f16)
-  static const bool tf32 = getenv("SEQREG_B200_NGFZ") && getenv("SEQREG_B200_NGFZ")[0] == '2';
-  // SEQREG_B200_NGFZN=1: 8-pixel items with every m-tile (k_ngf_z_f16n), for K <= 128 (2-D: MT = JT)
-  static const bool narrow = getenv("SEQREG_B200_NGFZN") && getenv("SEQREG_B200_NGFZN")[0] == '1';
-  if (!tf32 && narrow && D == 2 && JT > C::MW) {
-    const int KS = (K + 15) / 16;
-    const size_t smem = (size_t)2 * JT * KS * 32 * 16;
-    auto kern = JT <= 6 ? k_ngf_z_f16n<D, 6> : k_ngf_z_f16n<D, 8>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    const long long nblk8 = (nzp + 7) / 8;
-    const int grid = occupancy_grid(L, kern, 512, smem, (nblk8 + 15) / 16);
-    kern<<<grid, 512, smem, L.stream>>>(a, B.Nf, B.Rho, B.zlo, B.zhi, B.zstride, B.Z);
-    return cudaGetLastError();
-  }
-  if (!tf32) {
-    const int KS = (K + 15) / 16;
+  if (K > 128 || (long long)K * D * B.zstride >= (1LL << 31)) return cudaErrorNotSupported;
+  if (K <= 32) {  // legacy-pipe mma.sync f16 contraction (k_ngf_z_f16): C4 0.44 vs 0.82 ms for k_ngf_z_tc
+    using C = NZ<D>;
+    const int JT = (K + 15) / 16, KS = (K + 15) / 16;
+    const long long items = (nzp + C::PW - 1) / C::PW * ((JT + C::MW - 1) / C::MW);
     const size_t smem = (size_t)2 * JT * KS * 32 * 16;
     cudaError_t e = cudaFuncSetAttribute(k_ngf_z_f16<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -297,12 +283,14 @@ static cudaError_t run_ngf_z_mma(const Launch& L, const Args& a, const NgfBufs& 
     k_ngf_z_f16<D><<<grid, C::NT, smem, L.stream>>>(a, B.Nf, B.Rho, B.zlo, B.zhi, B.zstride, B.Z);
     return cudaGetLastError();
   }
-  const int KS = (K + 7) / 8;
-  const size_t smem = (size_t)2 * JT * KS * 32 * 16;
-  cudaError_t e = cudaFuncSetAttribute(k_ngf_z_mma<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const size_t smem = ztc_smem<D>(K);
+  cudaError_t e = cudaFuncSetAttribute(k_ngf_z_tc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const int grid = occupancy_grid(L, k_ngf_z_mma<D>, C::NT, smem, (items + C::NT / 32 - 1) / (C::NT / 32));
-  k_ngf_z_mma<D><<<grid, C::NT, smem, L.stream>>>(a, B.Nf, B.Rho, B.zlo, B.zhi, B.zstride, B.Z);
+  const int tp = ztc_mt((K + 15) / 16 * 16) * ZTC<D>::PXT;  // pixels per tile
+  const long long ntiles = (nzp + tp - 1) / tp;
+  int grid = L.grid_override > 0 ? L.grid_override : L.sms;
+  if (grid > ntiles) grid = (int)ntiles;
+  k_ngf_z_tc<D><<<grid, ZTC<D>::NT, smem, L.stream>>>(a, B.Nf, B.Rho, B.zlo, B.zhi, B.zstride, B.Z);
   return cudaGetLastError();
 }
 cudaError_t ngf_z_mma_d2(const Launch& L, const Args& a, const NgfBufs& B) { return run_ngf_z_mma<2>(L, a, B); }
