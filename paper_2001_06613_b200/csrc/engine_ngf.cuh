@@ -421,4 +421,184 @@ __global__ void __launch_bounds__(TGX<KP>::NT, 1) k_gram_tcx(const Args a, const
   }
 }
 
+
+// ------------------------------------------------------------------------------------------
+// 2-D sampling fused with the NGF feature (replaces k_sample_vp<LO> + k_ngf_feat4 and the u round trip):
+// CTA = (row segment, subset frame k), thread = 4 consecutive columns of every row (a whole image row per
+// CTA, so the x stencil needs no halo: neighbours come from the thread itself, its warp (shuffles) and the
+// next/previous warp (shared memory)).  Rows are walked in order with u of rows r - 1, r, r + 1 in
+// registers (fp64 values of the bilinear interpolant, grid.py:199-233) while the corner gathers of row
+// r + 2 and the y loads of row r + 3 are in flight, so a row's memory latency overlaps two rows of work.
+// At row r the thread writes n = grad_h u / rho and 1/rho (z rows [rz0, rz1)); grad T is written when
+// its row is sampled (slab rows [rs0, rs1)).  Same stencil as ngf_at (central differences inside,
+// one-sided at the domain edge, world units); the differences of u are taken in fp64 and rounded once.
+struct Corners2 {
+  float v00, v10, v01, v11, f0, f1;
+  bool inside;
+};
+template <bool POW2>
+__device__ __forceinline__ Corners2 fetch2(const float* __restrict__ img, const Geo& g, float px, float py) {
+  Corners2 c;
+  int base;
+  interp2_prep<float, POW2>(g, px, py, base, c.f0, c.f1, c.inside);
+  const float* q = img + base;
+  const int s1 = g.sti[1];
+  c.v00 = __ldg(q);
+  c.v10 = __ldg(q + 1);
+  c.v01 = __ldg(q + s1);
+  c.v11 = __ldg(q + s1 + 1);
+  return c;
+}
+// fp64 value and fp32 gradient (the arithmetic of interp_v64<2>)
+__device__ __forceinline__ double finish2(const Corners2& c, const Geo& g, bool pow2, float (&gr)[2]) {
+  const float d0 = c.v10 - c.v00, d1 = c.v11 - c.v01;
+  const float a0f = fmaf(c.f0, d0, c.v00), a1f = fmaf(c.f0, d1, c.v01);
+  const float gv0 = fmaf(c.f1, d1 - d0, d0), gv1 = a1f - a0f;
+  gr[0] = c.inside ? (pow2 ? gv0 * g.invf[0] : gv0 / g.sf[0]) : 0.f;
+  gr[1] = c.inside ? (pow2 ? gv1 * g.invf[1] : gv1 / g.sf[1]) : 0.f;
+  const double a0 = fma((double)c.f0, (double)c.v10 - (double)c.v00, (double)c.v00);
+  const double a1 = fma((double)c.f0, (double)c.v11 - (double)c.v01, (double)c.v01);
+  return c.inside ? fma((double)c.f1, a1 - a0, a0) : 0.0;
+}
+
+template <bool POW2>
+__global__ void __launch_bounds__(256, 2) k_ngf_sfeat2(const Args a, int seg, int rz0, int rz1, int rs0, int rs1,
+                                                       float* __restrict__ Nf, float* __restrict__ IRho,
+                                                       long long zlo, long long zstride, float* __restrict__ Gv,
+                                                       long long vlo, long long vstride) {
+  __shared__ double edge[2][2][32];  // [row parity][left / right edge][warp]
+  const int k = blockIdx.y;
+  const int n0 = a.g.n[0], n1 = a.g.n[1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int x0 = 4 * tid;
+  const bool colok = x0 < n0;
+  const int ra = rz0 + blockIdx.x * seg, rb = min(ra + seg, rz1);
+  if (ra >= rb) return;
+  const int fi = a.job->frame_index[k];
+  const float* img = reinterpret_cast<const float*>(a.frames) + (long long)fi * a.g.N;
+  const float* y0p = reinterpret_cast<const float*>(a.y) + (long long)(2 * k) * a.y_stride - a.y_off;
+  const float* y1p = y0p + a.y_stride;
+  const bool vec = (n0 & 3) == 0 && ((a.y_stride | a.y_off) & 3) == 0 &&
+                   (reinterpret_cast<uintptr_t>(a.y) & 15) == 0 && x0 + 4 <= n0;
+  const bool vz = vec && ((zlo | zstride) & 3) == 0, vg = vec && ((vlo | vstride) & 3) == 0;
+  const double h0 = 0.5 * a.g.inv[0], f0 = a.g.inv[0], h1 = 0.5 * a.g.inv[1], f1 = a.g.inv[1];
+  const float e = (float)a.eps, e2 = e * e;
+  float* gk0 = Gv + (long long)(2 * k) * vstride - vlo;
+  float* gk1 = gk0 + vstride;
+  auto load_y = [&](int r, float (&py)[4][2]) {
+    const long long pr = (long long)r * n0 + x0;
+    if (colok && vec) {
+      const float4 a0 = __ldg(reinterpret_cast<const float4*>(y0p + pr));
+      const float4 a1 = __ldg(reinterpret_cast<const float4*>(y1p + pr));
+      py[0][0] = a0.x, py[1][0] = a0.y, py[2][0] = a0.z, py[3][0] = a0.w;
+      py[0][1] = a1.x, py[1][1] = a1.y, py[2][1] = a1.z, py[3][1] = a1.w;
+    } else {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const bool ok = colok && x0 + t < n0;
+        py[t][0] = ok ? __ldg(y0p + pr + t) : 0.f;
+        py[t][1] = ok ? __ldg(y1p + pr + t) : 0.f;
+      }
+    }
+  };
+  auto fetch_row = [&](const float (&py)[4][2], Corners2 (&cr)[4]) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) cr[t] = fetch2<POW2>(img, a.g, py[t][0], py[t][1]);
+  };
+  // u of row r from its corners; grad T written when r is a slab row of this segment
+  auto finish_row = [&](int r, const Corners2 (&cr)[4], double (&u)[4]) {
+    float gt[4][2];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) u[t] = finish2(cr[t], a.g, POW2, gt[t]);
+    if (colok && r >= ra && r < rb && r >= rs0 && r < rs1) {
+      const long long q = (long long)r * n0 + x0;
+      if (vg) {
+        *reinterpret_cast<float4*>(gk0 + q) = make_float4(gt[0][0], gt[1][0], gt[2][0], gt[3][0]);
+        *reinterpret_cast<float4*>(gk1 + q) = make_float4(gt[0][1], gt[1][1], gt[2][1], gt[3][1]);
+      } else {
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          if (x0 + t < n0) {
+            gk0[q + t] = gt[t][0];
+            gk1[q + t] = gt[t][1];
+          }
+      }
+    }
+  };
+  // prologue: u of rows ra - 1, ra, ra + 1 in registers, corners of ra + 2 and y of ra + 3 in flight
+  double um[4] = {0, 0, 0, 0}, uc[4], up[4] = {0, 0, 0, 0};
+  float yv[4][2];
+  Corners2 cr[4];
+  if (ra > 0) {
+    load_y(ra - 1, yv);
+    fetch_row(yv, cr);
+    finish_row(ra - 1, cr, um);
+  }
+  load_y(ra, yv);
+  fetch_row(yv, cr);
+  finish_row(ra, cr, uc);
+  if (ra + 1 < n1) {
+    load_y(ra + 1, yv);
+    fetch_row(yv, cr);
+    finish_row(ra + 1, cr, up);
+  }
+  const int rlast = min(rb, n1 - 1);  // last row ever sampled by this segment
+  if (ra + 2 <= rlast) load_y(ra + 2, yv);
+  for (int r = ra; r < rb; ++r) {
+    const int par = r & 1;
+    const bool more = r + 2 <= rlast;
+    if (more) fetch_row(yv, cr);                  // corners of row r + 2 (in flight during row r)
+    if (r + 3 <= rlast) load_y(r + 3, yv);        // y of row r + 3
+    if (lane == 0) edge[par][1][warp] = uc[0];
+    if (lane == 31) edge[par][0][warp] = uc[3];
+    __syncthreads();
+    double left = __shfl_up_sync(0xffffffffu, uc[3], 1), right = __shfl_down_sync(0xffffffffu, uc[0], 1);
+    if (lane == 0) left = warp > 0 ? edge[par][0][warp - 1] : uc[0];
+    if (lane == 31) right = warp + 1 < nw ? edge[par][1][warp + 1] : uc[3];
+    const bool c1 = r > 0 && r + 1 < n1;
+    float nv[2][4], irv[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int x = x0 + t;
+      const double ul = t == 0 ? left : uc[t - 1], ur = t == 3 ? right : uc[t + 1];
+      const bool hm = x > 0, hp = x < n0 - 1;
+      const double dxl = hm ? ul : uc[t], dxr = hp ? ur : uc[t];
+      const double dyl = r > 0 ? um[t] : uc[t], dyr = r + 1 < n1 ? up[t] : uc[t];
+      const float g0 = (float)((dxr - dxl) * ((hm && hp) ? h0 : f0));
+      const float g1 = (float)((dyr - dyl) * (c1 ? h1 : f1));
+      const float rho = sqrtf(g0 * g0 + g1 * g1 + e2);
+      const float ir = 1.f / rho;
+      nv[0][t] = g0 * ir;
+      nv[1][t] = g1 * ir;
+      irv[t] = ir;
+    }
+    if (colok) {
+      const long long q = (long long)r * n0 + x0;
+      float* n0p = Nf + (long long)(2 * k) * zstride + (q - zlo);
+      float* n1p = n0p + zstride;
+      float* irp = IRho + (long long)k * zstride + (q - zlo);
+      if (vz) {
+        *reinterpret_cast<float4*>(n0p) = make_float4(nv[0][0], nv[0][1], nv[0][2], nv[0][3]);
+        *reinterpret_cast<float4*>(n1p) = make_float4(nv[1][0], nv[1][1], nv[1][2], nv[1][3]);
+        *reinterpret_cast<float4*>(irp) = make_float4(irv[0], irv[1], irv[2], irv[3]);
+      } else {
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          if (x0 + t < n0) {
+            n0p[t] = nv[0][t];
+            n1p[t] = nv[1][t];
+            irp[t] = irv[t];
+          }
+      }
+    }
+    double un[4];
+    if (more) finish_row(r + 2, cr, un);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      um[t] = uc[t];
+      uc[t] = up[t];
+      up[t] = more ? un[t] : up[t];
+    }
+  }
+}
 }  // namespace sr

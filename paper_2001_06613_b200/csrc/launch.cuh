@@ -297,6 +297,27 @@ struct NgfBufs {
   long long vlo, vhi, vstride, zlo, zhi, zstride;
 };
 
+// 2-D fused sampling + NGF feature (k_ngf_sfeat2) over the NgfBufs ranges; NotSupported when a row does
+// not fit one CTA (n0 > 1024) or the ranges are not whole rows
+inline cudaError_t ngf_sfeat_d2(const Launch& L, const Args& a, const NgfBufs& B) {
+  const int n0 = a.g.n[0];
+  if (a.g.nd != 2 || n0 > 1024 || (B.zlo % n0) || (B.zhi % n0) || (a.pix_lo % n0) || (a.pix_hi % n0))
+    return cudaErrorNotSupported;
+  const int rz0 = (int)(B.zlo / n0), rz1 = (int)(B.zhi / n0);
+  const int rs0 = (int)(a.pix_lo / n0), rs1 = (int)(a.pix_hi / n0);
+  int seg = 32;
+  while (seg > 8 && (long long)((rz1 - rz0 + seg - 1) / seg) * a.K < 8LL * L.sms) seg /= 2;
+  const dim3 grid((unsigned)((rz1 - rz0 + seg - 1) / seg), (unsigned)a.K);
+  const int nt = ((n0 + 3) / 4 + 31) / 32 * 32;
+  if (a.g.pow2)
+    k_ngf_sfeat2<true><<<grid, nt, 0, L.stream>>>(a, seg, rz0, rz1, rs0, rs1, B.Nf, B.Rho, B.zlo, B.zstride, B.G,
+                                                  B.vlo, B.vstride);
+  else
+    k_ngf_sfeat2<false><<<grid, nt, 0, L.stream>>>(a, seg, rz0, rz1, rs0, rs1, B.Nf, B.Rho, B.zlo, B.zstride, B.G,
+                                                   B.vlo, B.vstride);
+  return cudaGetLastError();
+}
+
 template <int D, int KP>
 cudaError_t run_ngf_pass1_kp(const Launch& L, const Args& a, const NgfBufs& B, double* part, size_t part_cap,
                              int* nblk) {
@@ -317,17 +338,20 @@ cudaError_t run_ngf_pass1_kp(const Launch& L, const Args& a, const NgfBufs& B, d
          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorNotSupported;
-  // u and grad T over [vlo, vhi) (no shift: n only sees differences of u)
-  Args av = a;
-  av.pix_lo = B.vlo;
-  av.pix_hi = B.vhi;
-  av.shifts = nullptr;
-  cudaError_t e = D == 2 ? sample_vg_d2(L, av, B.V, B.G, B.vstride, B.VL)
-                         : sample_vg_d3(L, av, B.V, B.G, B.vstride, B.VL);
-  if (e != cudaSuccess) return e;
-  const dim3 fgrid((unsigned)((B.zhi - B.zlo + 1023) / 1024), (unsigned)a.K);
-  k_ngf_feat4<D><<<fgrid, 256, 0, L.stream>>>(a, B.V, B.VL, B.vlo, B.vstride, B.Nf, B.Rho, B.zlo, B.zhi, B.zstride);
-  e = cudaGetLastError();
+  cudaError_t e = D == 2 ? ngf_sfeat_d2(L, a, B) : cudaErrorNotSupported;
+  if (e == cudaErrorNotSupported) {
+    // u (an fp32 pair) and grad T over [vlo, vhi) (no shift: n only sees differences of u), then n, 1/rho
+    Args av = a;
+    av.pix_lo = B.vlo;
+    av.pix_hi = B.vhi;
+    av.shifts = nullptr;
+    e = D == 2 ? sample_vg_d2(L, av, B.V, B.G, B.vstride, B.VL) : sample_vg_d3(L, av, B.V, B.G, B.vstride, B.VL);
+    if (e != cudaSuccess) return e;
+    const dim3 fgrid((unsigned)((B.zhi - B.zlo + 1023) / 1024), (unsigned)a.K);
+    k_ngf_feat4<D><<<fgrid, 256, 0, L.stream>>>(a, B.V, B.VL, B.vlo, B.vstride, B.Nf, B.Rho, B.zlo, B.zhi,
+                                                B.zstride);
+    e = cudaGetLastError();
+  }
   if (e != cudaSuccess) return e;
   const size_t smem = tgx_smem<KP>();
   e = cudaFuncSetAttribute(k_gram_tcx<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -157,11 +157,15 @@ static cudaError_t run_ngf_pass1_mma(const Launch& L, const Args& a, const NgfBu
   av.pix_lo = B.vlo;
   av.pix_hi = B.vhi;
   av.shifts = nullptr;
-  cudaError_t e = launch_sample_vg<D>(L, av, B.V, B.G, B.vstride, B.VL);
-  if (e != cudaSuccess) return e;
-  const dim3 fgrid((unsigned)((B.zhi - B.zlo + 1023) / 1024), (unsigned)a.K);
-  k_ngf_feat4<D><<<fgrid, 256, 0, L.stream>>>(a, B.V, B.VL, B.vlo, B.vstride, B.Nf, B.Rho, B.zlo, B.zhi, B.zstride);
-  e = cudaGetLastError();
+  cudaError_t e = D == 2 ? ngf_sfeat_d2(L, a, B) : cudaErrorNotSupported;
+  if (e == cudaErrorNotSupported) {
+    e = launch_sample_vg<D>(L, av, B.V, B.G, B.vstride, B.VL);
+    if (e != cudaSuccess) return e;
+    const dim3 fgrid((unsigned)((B.zhi - B.zlo + 1023) / 1024), (unsigned)a.K);
+    k_ngf_feat4<D><<<fgrid, 256, 0, L.stream>>>(a, B.V, B.VL, B.vlo, B.vstride, B.Nf, B.Rho, B.zlo, B.zhi,
+                                                B.zstride);
+    e = cudaGetLastError();
+  }
   if (e != cudaSuccess) return e;
   const int sup = gram_sup();
   const size_t smem = gtm_smem(sup);
