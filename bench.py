@@ -444,6 +444,103 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+PIPELINES = {
+    # BASELINE configs[0] and configs[4]: the full spatio-temporal multilevel run (multilevel.field_stml_run)
+    "c1": dict(spatial_levels=3, temporal_coarsest_size=4, iters=20),
+    "c5": dict(spatial_levels=4, temporal_coarsest_size=9, iters=10),
+}
+
+
+def run_pipeline(args):
+    """--pipeline: the end-to-end multilevel registration of C1 / C5 on one GPU.  A step is one whole run
+    (every spatial x temporal level, fixed L-BFGS iterations) from the frames in pinned host memory to the
+    final fields back in host memory; ``value`` counts the voxel-frames of every objective evaluation of
+    the run per second of the run.  The final all-frames D is checked against the CPU oracle evaluated at
+    the GPU's final fields (fp64 arithmetic on the same inputs)."""
+    import torch
+
+    import paper_2001_06613_b200 as srb
+    from paper_2001_06613_b200 import multilevel as ml
+    from paper_2001_06613_b200 import synth
+    from paper_2001_06613_b200.optimizer import OptimOptions
+
+    name = args.config
+    if name not in PIPELINES:
+        raise SystemExit(f"--pipeline runs {sorted(PIPELINES)}")
+    pc = PIPELINES[name]
+    cfg = synth.CONFIGS[name]
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    frames, times, spacing, origin = synth.make_sequence(cfg, seed=0, device=dev)
+    host = frames.to(cfg.dtype).cpu().pin_memory()
+    del frames
+    fcfg = ml.FieldRunConfig(spatial_levels=pc["spatial_levels"], temporal_coarsest_size=pc["temporal_coarsest_size"],
+                             feature=cfg.feature, ngf_eps=cfg.ngf_eps, alpha=cfg.alpha, weights="uniform", eps=None,
+                             optim=OptimOptions(max_iters=pc["iters"], grad_tol=1e-30, f_tol=1e-30, step_tol=1e-30))
+    eng = srb.get_engine(0)
+    grid = srb.GridSpec(cfg.dims, spacing, origin)
+
+    def one_run():
+        fd = srb.DeviceFrames(eng, host.to(dev, non_blocking=True), grid)
+        y, runs = ml.field_stml_run(fd, times, fcfg)
+        y_host = y.cpu()
+        return y_host, runs
+
+    for _ in range(max(1, args.warmup)):
+        one_run()
+    torch.cuda.synchronize()
+    walls, last = [], None
+    sampler = ClockSampler(0)
+    with sampler:
+        t_all = time.perf_counter()
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            last = one_run()
+            walls.append(time.perf_counter() - t0)
+        sampler.window = (t_all, time.perf_counter())
+    y_host, runs = last
+    # voxel-frames evaluated per run: every objective evaluation of every solve + the all-frames scores
+    levels_n = []
+    dims = tuple(cfg.dims)
+    for _ in range(pc["spatial_levels"]):
+        levels_n.insert(0, int(np.prod(dims)))
+        dims = tuple(-(-d // 2) for d in dims)
+    vf = sum(levels_n[r.spatial_level] * (len(r.active) * r.evaluations + cfg.K) for r in runs)
+    wall = float(np.median(walls))
+    # final D against the oracle at the same fields (finest level, all frames, fp64 arithmetic)
+    from oracle import seqreg_oracle as orc
+
+    t0 = time.perf_counter()
+    fr = host.double().numpy()
+    _st, d_ref, _g = orc.evaluate_field(list(fr), cfg.dims, spacing, origin, y_host.double().numpy(),
+                                        np.full(cfg.K, 1.0 / cfg.K), float(np.prod(spacing)), cfg.feature,
+                                        cfg.ngf_eps, threads=os.cpu_count() or 8)
+    oracle_s = time.perf_counter() - t0
+    d_gpu = runs[-1].dissim_all
+    nbytes_in = int(host.numel() * host.element_size())
+    line = {
+        "metric": METRIC, "value": vf / wall, "unit": "voxel-frames/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": wall * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32" if cfg.dtype.itemsize == 4 else "f64",
+        "data": "synthetic (seeded Gaussian-blob sequence + sinusoidal motion, BASELINE.json generator)",
+        "config": {"workload": f"{name}: end-to-end multilevel run, {pc['spatial_levels']} spatial x "
+                               f"{len(ml.temporal_levels(cfg.K, pc['temporal_coarsest_size']))} temporal levels, "
+                               f"{pc['iters']} L-BFGS iterations per level, K={cfg.K} "
+                               f"{'x'.join(map(str, cfg.dims))} {cfg.feature.upper()} alpha={cfg.alpha}",
+                   "step": "one whole run: H2D of the frames, pyramid, every solve, D2H of the final fields"},
+        "pipeline": {"runs": [{"level": [r.spatial_level, r.temporal_level], "frames": len(r.active),
+                               "iterations": r.iterations, "evaluations": r.evaluations, "reason": r.reason,
+                               "f_final": r.f_final, "dissim_all": r.dissim_all, "ms": r.wall_ms} for r in runs],
+                     "voxel_frames_evaluated": vf, "wall_s": walls,
+                     "final_D": d_gpu, "final_D_oracle": d_ref, "final_D_rel_err": abs(d_gpu - d_ref) / abs(d_ref),
+                     "oracle_eval_s": oracle_s},
+        "e2e": {"value": vf / wall, "unit": "voxel-frames/s", "h2d_bytes_per_step": nbytes_in,
+                "d2h_bytes_per_step": int(y_host.numel() * y_host.element_size()), "ms_per_step": wall * 1e3},
+        "clocks": sampler.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def run_dry(args):
     """CPU check of the multi-rank plumbing: every rank joins a gloo group, takes its slab of the config
     and checks the all-gather; rank 0 prints the line skeleton with n_gpus."""
@@ -490,6 +587,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-budget", type=float, default=120.0)
     ap.add_argument("--dry-run", action="store_true")
+    ap.add_argument("--pipeline", action="store_true", help="c1/c5: the end-to-end multilevel run")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # one rank per GPU: re-launch under torchrun (the driver launches torchrun itself; this is for
@@ -500,6 +598,8 @@ def main():
         sys.exit(subprocess.call(cmd))
     if args.dry_run:
         run_dry(args)
+    elif args.pipeline:
+        run_pipeline(args)
     elif args.impl == "reference":
         run_reference(args)
     else:

@@ -37,7 +37,7 @@ from .spatial import build_pyramid, prolong_field
 from .temporal import interp_linear_fields, ls_predict_fields
 
 __all__ = ["FieldRunConfig", "FieldLevelRun", "temporal_levels", "default_time_interval", "quad_weights",
-           "field_stml_run"]
+           "precondition_scale", "field_stml_run"]
 
 
 def temporal_levels(n: int, coarsest_size: int) -> list:
@@ -94,6 +94,11 @@ class FieldRunConfig:
     # iterations, line_search_failure) and the run is not reproducible to rounding.  0.3 cells stays off the
     # nodes after prolongation too (0.6, 1.2, 2.4 cells on the finer levels).  0 restores the identity.
     start_offset: float = 0.3
+    # Preconditioned coordinates (the field analogue of _gir_solve's scale, temporal.py:320-325): the solver
+    # sees x = y / c with c^2 = 1 / lambda_max(alpha h L^T L) = s^4 / (alpha h (4 d)^2) (s the smallest
+    # spacing), so its unit first step (p = -g, optimizer.py:104) is stable for the stiffest curvature mode;
+    # without it every C5 solve (alpha = 10) ends in line_search_failure at iteration 0.  c = 1 when alpha = 0.
+    precondition: bool = True
 
     def __post_init__(self):
         if self.spatial_levels < 1:
@@ -143,23 +148,36 @@ def _identity(grid, n: int, dtype, device, offset: float = 0.0) -> torch.Tensor:
     return torch.as_tensor(x, dtype=dtype, device=device).unsqueeze(0).expand(n, -1, -1).contiguous()
 
 
+def precondition_scale(grid, alpha: float) -> float:
+    """c of FieldRunConfig.precondition: c^2 = s^4 / (alpha h (4 d)^2), 1 without the regulariser."""
+    if alpha <= 0:
+        return 1.0
+    s = min(grid.spacing)
+    return float(s * s / (4 * grid.ndim * np.sqrt(alpha * grid.cell_volume)))
+
+
 def _solve(lvl: DeviceFrames, subset, init: torch.Tensor, w, cfg: FieldRunConfig):
-    """_gir_solve (temporal.py:304-341) for displacement fields: J = D + S over the subset."""
+    """_gir_solve (temporal.py:304-341) for displacement fields: J = D + S over the subset, in the
+    preconditioned coordinates x = y / c."""
     obj = FieldObjective(lvl, list(subset), w, feature=cfg.feature, ngf_eps=cfg.ngf_eps, alpha=cfg.alpha)
     shape = obj.shape
     dt = lvl.dtype
+    c = precondition_scale(lvl.grid, cfg.alpha) if cfg.precondition else 1.0
     y = torch.empty(shape, dtype=dt, device=lvl.data.device)
     g = torch.empty(shape, dtype=dt, device=lvl.data.device)
 
     def objective(x: torch.Tensor) -> ObjectiveEval:
-        y.copy_(x.view(shape))
+        y.copy_(x.view(shape) * c if c != 1.0 else x.view(shape))
         stats, _ = obj.evaluate(y, g)
         value = stats[0] + obj.s_reg[0] if cfg.alpha > 0 else stats[0]
-        return ObjectiveEval(float(value.item()), g.reshape(-1))
+        grad = g.reshape(-1).to(torch.float64)
+        return ObjectiveEval(float(value.item()), grad * c if c != 1.0 else grad)
 
-    x0 = init.to(torch.float64).reshape(-1).contiguous()
+    x0 = init.to(torch.float64).reshape(-1)
+    x0 = (x0 / c if c != 1.0 else x0).contiguous()
     res = lbfgs_minimize(objective, x0, cfg.optim, engine=lvl.engine)
-    return res.x_final.view(shape).to(dt), res
+    xf = res.x_final.view(shape)
+    return (xf * c if c != 1.0 else xf).to(dt), res
 
 
 def _dissim_all(lvl: DeviceFrames, y_all: torch.Tensor, w_all, cfg: FieldRunConfig) -> float:

@@ -64,7 +64,7 @@ def test_c1_each_solve_matches_oracle(c1_run):
         h = float(np.prod(lsp))
         w = np.full(len(r.active), 1.0 / len(fr))
         y0 = r.y_init.cpu().numpy()
-        y1, q = orc.field_solve([lf[k] for k in r.active], dm, lsp, org, y0, w, h, "ngf", 0.1, alpha, ITERS, 8)
+        y1, q = orc.field_solve([lf[k] for k in r.active], dm, lsp, org, y0, w, h, "ngf", 0.1, alpha, ITERS, 8, True)
         assert (r.iterations, r.evaluations, r.reason) == (q["iterations"], q["objective_evaluations"],
                                                            q["converged_reason"]), (r.spatial_level, r.temporal_level)
         fscale = abs(q["f_initial"])
