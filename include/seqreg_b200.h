@@ -20,6 +20,7 @@
  *   sr_grad           re-warp + chain rule back to y or to the affine
  *                     parameters                                    (similarity.py:203-220, grid.py:246-253)
  *   sr_curvature      curvature regulariser S(y) and its gradient   (absent in the reference)
+ *   sr_evaluate_reg   sr_evaluate + S(y) (fused into pass 2 on the split NGF path)
  *   sr_ls_predict     temporal prolongation: smoothing least squares
  *                     with a shared tridiagonal matrix               (temporal.py:194-239, thomas_solve 166-191)
  *   sr_interp_linear  temporal prolongation at the coarsest level    (temporal.py:109-127)
@@ -178,6 +179,14 @@ SR_API int sr_grad(sr_ctx* ctx, const sr_problem* prob, const double* stats_dev,
  * stats_dev[0]; grad_dev may be NULL for a D-only evaluation (temporal.py:297-301). */
 SR_API int sr_evaluate(sr_ctx* ctx, const sr_problem* prob, const double* weights, double cell_volume,
                 double* raw_dev, double* stats_dev, void* grad_dev);
+
+/* sr_evaluate plus the curvature regulariser S(y) (alpha > 0, displacement fields): the gradient gets
+ * alpha h L L (y - x) added and S goes to s_out_dev[0].  The split fp32 NGF path adds the term inside its
+ * pass-2 kernel (one launch, no read-modify-write of grad); every other path runs sr_curvature's kernel
+ * after pass 2.  alpha = 0 is sr_evaluate.  (J = D + S, temporal.py:334-336 with S in place of the
+ * affine drift penalty; north_star kernel 4.) */
+SR_API int sr_evaluate_reg(sr_ctx* ctx, const sr_problem* prob, const double* weights, double cell_volume,
+                    double alpha, double* raw_dev, double* stats_dev, void* grad_dev, double* s_out_dev);
 
 /* Curvature regulariser on displacement fields:
  *   S = alpha/2 * h * sum_{j,c} || L (y_jc - x_c) ||^2,  grad += alpha * h * L L (y - x),

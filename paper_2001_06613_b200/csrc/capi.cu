@@ -95,6 +95,12 @@ struct sr_ctx {
   size_t zbuf_bytes = 0;
   double* aux = nullptr;  // small device scratch (temporal factors, S partial reduce)
   size_t aux_cap = 0;
+  // curvature regulariser of the current sr_evaluate_reg call (alpha > 0): pass 2 adds alpha h L L (y - x)
+  // to the gradient and writes S to curv_s (one double)
+  double curv_alpha = 0.0, curv_h = 0.0;
+  double* curv_s = nullptr;
+  double* curv_part = nullptr;
+  size_t curv_part_cap = 0;
   int* iaux = nullptr;
   size_t iaux_cap = 0;
   std::vector<TexSet> texsets;
@@ -558,6 +564,7 @@ int sr_destroy(sr_ctx* c) {
   cudaFreeHost(c->job_host);
   cudaFree(c->part);
   cudaFree(c->ticket);
+  cudaFree(c->curv_part);
   sr::lbfgs::destroy(c->lbfgs);
   cudaFree(c->vbuf);
   cudaFree(c->gbuf);
@@ -702,8 +709,12 @@ int sr_corr_finalize(sr_ctx* c, const sr_problem* p, const double* raw_dev, cons
   return finalize_impl(c, p, raw_dev, cell_volume, n_total, stats_dev);
 }
 
-static int grad_impl(sr_ctx* c, const sr_problem* p, const double* stats, void* grad, int64_t g_off,
-                     int64_t g_stride, bool reuse) {
+static int curvature_impl(sr_ctx* c, const sr_problem* p, double alpha, double h, void* grad, int64_t g_off,
+                          int64_t g_stride, double* s_out);
+
+// bool *curv_done: the pass-2 kernel added the curvature term itself (the split NGF path)
+static int grad_impl_core(sr_ctx* c, const sr_problem* p, const double* stats, void* grad, int64_t g_off,
+                          int64_t g_stride, bool reuse, bool* curv_done) {
   const int KP = kp_of(p->k);
   const int d = p->grid.ndim, na = d * d + d;
   const Launch L = launch_of(c);
@@ -743,7 +754,22 @@ static int grad_impl(sr_ctx* c, const sr_problem* p, const double* stats, void* 
     a.out = grad;
     a.o_off = g_off;
     a.o_stride = g_stride;
+    const bool fuse = c->curv_alpha > 0 && p->param == SR_DISPLACEMENT && p->dtype == SR_F32;
+    int nb = 0;
+    if (fuse) {  // the curvature term inside k_ngf_adj4 (one pass-2 launch, no read-modify-write of grad)
+      nb = (int)((npix + 1023) / 1024) * p->k;
+      rc = ensure_d(&c->curv_part, &c->curv_part_cap, (size_t)nb);
+      if (rc) return rc;
+      a.curv_alpha = c->curv_alpha;
+      a.curv_h = c->curv_h;
+      a.curv_part = c->curv_part;
+    }
     CK(d == 2 ? ngf_pass2_d2(L, a, c->vtag.ngf) : ngf_pass2_d3(L, a, c->vtag.ngf));
+    if (fuse) {
+      k_reduce<<<1, 256, 0, c->stream>>>(c->curv_part, nb, 1, 1, 1, 1, c->curv_s);
+      CK(cudaGetLastError());
+      *curv_done = true;
+    }
     return SR_OK;
   }
   // NGF: z over the slab extended by one slowest-axis row on each side (the adjoint stencil)
@@ -771,6 +797,15 @@ static int grad_impl(sr_ctx* c, const sr_problem* p, const double* stats, void* 
     CK(cudaGetLastError());
   }
   return SR_OK;
+}
+
+static int grad_impl(sr_ctx* c, const sr_problem* p, const double* stats, void* grad, int64_t g_off,
+                     int64_t g_stride, bool reuse) {
+  bool done = false;
+  int rc = grad_impl_core(c, p, stats, grad, g_off, g_stride, reuse, &done);
+  if (rc || done || !(c->curv_alpha > 0) || p->param != SR_DISPLACEMENT) return rc;
+  // every other pass 2: the curvature kernel after it (adds into grad)
+  return curvature_impl(c, p, c->curv_alpha, c->curv_h, grad, g_off, g_stride, c->curv_s);
 }
 
 int sr_grad(sr_ctx* c, const sr_problem* p, const double* stats_dev, void* grad_dev, int64_t g_off,
@@ -817,6 +852,34 @@ static std::vector<unsigned char> eval_key(const sr_problem* p, const double* we
   return k;
 }
 
+static void key_put_curv(std::vector<unsigned char>& k, const sr_ctx* c) {
+  const unsigned char* b = reinterpret_cast<const unsigned char*>(&c->curv_alpha);
+  k.insert(k.end(), b, b + sizeof(double));
+  b = reinterpret_cast<const unsigned char*>(&c->curv_h);
+  k.insert(k.end(), b, b + sizeof(double));
+  b = reinterpret_cast<const unsigned char*>(&c->curv_s);
+  k.insert(k.end(), b, b + sizeof(double*));
+}
+
+int sr_evaluate_reg(sr_ctx* c, const sr_problem* p, const double* weights, double cell_volume, double alpha,
+                    double* raw_dev, double* stats_dev, void* grad_dev, double* s_out_dev) {
+  if (!c) return fail(SR_ERR_ARG, "null context");
+  if (alpha > 0) {
+    if (!p || p->param != SR_DISPLACEMENT) return fail(SR_ERR_ARG, "the curvature regulariser acts on displacement fields");
+    if (!grad_dev || !s_out_dev) return fail(SR_ERR_ARG, "null grad/s_out");
+  } else if (alpha < 0 || alpha != alpha) {
+    return fail(SR_ERR_ARG, "alpha must be >= 0");
+  }
+  c->curv_alpha = alpha > 0 ? alpha : 0.0;
+  c->curv_h = alpha > 0 ? cell_volume : 0.0;
+  c->curv_s = alpha > 0 ? s_out_dev : nullptr;
+  const int rc = sr_evaluate(c, p, weights, cell_volume, raw_dev, stats_dev, grad_dev);
+  c->curv_alpha = 0.0;
+  c->curv_h = 0.0;
+  c->curv_s = nullptr;
+  return rc;
+}
+
 int sr_evaluate(sr_ctx* c, const sr_problem* p, const double* weights, double cell_volume,
                 double* raw_dev, double* stats_dev, void* grad_dev) {
   int rc = check_problem(c, p);
@@ -835,7 +898,8 @@ int sr_evaluate(sr_ctx* c, const sr_problem* p, const double* weights, double ce
   // CUDA-graph replay of a repeated evaluation (the objective inside an optimiser loop): one graph
   // launch instead of the per-kernel launches.  A key is captured on its second evaluation (the first
   // runs eagerly and sizes every scratch buffer); the graph reads its own device copy of the Job.
-  const std::vector<unsigned char> key = eval_key(p, weights, cell_volume, raw_dev, stats_dev, grad_dev);
+  std::vector<unsigned char> key = eval_key(p, weights, cell_volume, raw_dev, stats_dev, grad_dev);
+  key_put_curv(key, c);
   sr_ctx::EvalGraph* eg = nullptr;
   for (auto& e : c->egraphs)
     if (e.key == key) eg = &e;
@@ -917,6 +981,12 @@ int sr_curvature(sr_ctx* c, const sr_problem* p, double alpha, double h, void* g
   if (p->param != SR_DISPLACEMENT) return fail(SR_ERR_ARG, "the curvature regulariser acts on displacement fields");
   if (!grad || !s_out) return fail(SR_ERR_ARG, "null grad/s_out");
   CK(cudaSetDevice(c->device));
+  return curvature_impl(c, p, alpha, h, grad, g_off, g_stride, s_out);
+}
+
+static int curvature_impl(sr_ctx* c, const sr_problem* p, double alpha, double h, void* grad, int64_t g_off,
+                          int64_t g_stride, double* s_out) {
+  int rc = SR_OK;
   const int d = p->grid.ndim;
   const long long npix = p->pix_hi - p->pix_lo;
   const size_t need = (size_t)((npix + 255) / 256 + 1) * p->k * d;

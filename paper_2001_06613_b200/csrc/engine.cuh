@@ -44,6 +44,9 @@ struct Args {
   int dbg;              // SEQREG_B200_DEBUG bits (profiling experiments only)
   int ymap_ok;          // a y tensor map was encoded for the warp-specialized kernels
   int use_tex;          // job->tex[] holds gather textures of the subset frames (fp32)
+  double curv_alpha;    // > 0: pass 2 adds the curvature gradient alpha h L L (y - x) (sr_evaluate_reg)
+  double curv_h;
+  double* curv_part;    // per-CTA partial sums of S (reduced by k_reduce)
 };
 
 // --------------------------------------------------------- stats buffer layout
@@ -1232,6 +1235,32 @@ __device__ __forceinline__ double lap_u(const Args& a, const T* __restrict__ yc,
     out += (up - 2.0 * u0 + um) * a.g.inv[ax] * a.g.inv[ax];
   }
   return out;
+}
+
+// alpha h (L L u)(pix) for u = y - x of one component (the arithmetic of k_curvature); adds this
+// pixel's 1/2 alpha h (L u)^2 to *sval
+template <typename T, int D>
+__device__ __forceinline__ double curv_grad_at(const Args& a, const T* __restrict__ yc, int comp, long long pix,
+                                               const int (&c)[3], double alpha, double h, double& sval) {
+  const double l0 = lap_u<T, D>(a, yc, comp, pix, c);
+  sval += 0.5 * alpha * h * l0 * l0;
+  double ll = 0.0;
+#pragma unroll
+  for (int ax = 0; ax < D; ++ax) {
+    double lp = l0, lm = l0;
+    if (c[ax] < a.g.n[ax] - 1) {
+      int cc[3] = {c[0], c[1], c[2]};
+      cc[ax] += 1;
+      lp = lap_u<T, D>(a, yc, comp, pix + a.g.st[ax], cc);
+    }
+    if (c[ax] > 0) {
+      int cc[3] = {c[0], c[1], c[2]};
+      cc[ax] -= 1;
+      lm = lap_u<T, D>(a, yc, comp, pix - a.g.st[ax], cc);
+    }
+    ll += (lp - 2.0 * l0 + lm) * a.g.inv[ax] * a.g.inv[ax];
+  }
+  return alpha * h * ll;
 }
 
 template <typename T, int D>

@@ -133,14 +133,19 @@ __global__ void __launch_bounds__(256) k_ngf_feat4(const Args a, const float* __
 
 // dD/dy = (D_h^T z) grad T, 4 consecutive pixels per thread (same arithmetic as dgrad_adjoint), 128-bit
 // grad T loads and dD/dy stores when aligned.
-template <int D>
+// CURV (sr_evaluate_reg): the curvature gradient alpha h L L (y - x) of the same pixels is added to the
+// output in the same launch (same arithmetic and the same float addition as k_curvature after this kernel),
+// and the CTA's share of S goes to a.curv_part[blockIdx.y * gridDim.x + blockIdx.x].
+template <int D, bool CURV = false>
 __global__ void __launch_bounds__(256) k_ngf_adj4(const Args a, const float* __restrict__ Z, long long zlo,
                                                   long long zstride, const float* __restrict__ Gv, long long vlo,
                                                   long long vstride) {
   const int k = blockIdx.y;
   const int npix = (int)(a.pix_hi - a.pix_lo);
   const int q0 = (blockIdx.x * 256 + threadIdx.x) * 4;  // slab-relative first pixel
-  if (q0 >= npix) return;
+  if (!CURV && q0 >= npix) return;
+  double sval = 0.0;
+  if (q0 < npix) {
   const int p0 = (int)a.pix_lo + q0;
   int c[3];
   coords_flat(a.g, p0, c);
@@ -214,13 +219,48 @@ __global__ void __launch_bounds__(256) k_ngf_adj4(const Args a, const float* __r
   for (int cc = 0; cc < D; ++cc) {
     const float* gs = Gv + ((long long)k * D + cc) * vstride + go;
     float* dst = out + ((long long)k * D + cc) * a.o_stride + oo;
+    float cv[4] = {0.f, 0.f, 0.f, 0.f};
+    if (CURV) {
+      const float* yc = reinterpret_cast<const float*>(a.y) + (long long)(k * D + cc) * a.y_stride;
+      int cq[3];
+      coords_flat(a.g, p0, cq);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        if (q0 + t < npix) cv[t] = (float)curv_grad_at<float, D>(a, yc, cc, p0 + t, cq, a.curv_alpha, a.curv_h, sval);
+        if (++cq[0] == a.g.n[0]) {
+          cq[0] = 0;
+          if (D > 1 && ++cq[1] == a.g.n[1]) {
+            cq[1] = 0;
+            ++cq[2];
+          }
+        }
+      }
+    }
     if (vec) {
       const float4 gv = __ldg(reinterpret_cast<const float4*>(gs));
-      *reinterpret_cast<float4*>(dst) = make_float4(du[0] * gv.x, du[1] * gv.y, du[2] * gv.z, du[3] * gv.w);
+      float4 o = make_float4(du[0] * gv.x, du[1] * gv.y, du[2] * gv.z, du[3] * gv.w);
+      if (CURV) o.x += cv[0], o.y += cv[1], o.z += cv[2], o.w += cv[3];
+      *reinterpret_cast<float4*>(dst) = o;
     } else {
 #pragma unroll
       for (int t = 0; t < 4; ++t)
-        if (q0 + t < npix) dst[t] = du[t] * __ldg(gs + t);
+        if (q0 + t < npix) {
+          float o = du[t] * __ldg(gs + t);
+          if (CURV) o += cv[t];
+          dst[t] = o;
+        }
+    }
+  }
+  }  // q0 < npix
+  if (CURV) {
+    __shared__ double red[8];
+    const double v = warp_sum(sval);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int w = 0; w < 8; ++w) s += red[w];
+      a.curv_part[(size_t)blockIdx.y * gridDim.x + blockIdx.x] = s;
     }
   }
 }

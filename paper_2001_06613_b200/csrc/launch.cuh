@@ -385,7 +385,10 @@ cudaError_t run_ngf_pass2(const Launch& L, const Args& a, const NgfBufs& B) {
   const cudaError_t ez = D == 2 ? ngf_z_mma_d2(L, a, B) : ngf_z_mma_d3(L, a, B);
   if (ez != cudaSuccess) return ez;
   const dim3 g2((unsigned)((a.pix_hi - a.pix_lo + 1023) / 1024), (unsigned)a.K);
-  k_ngf_adj4<D><<<g2, 256, 0, L.stream>>>(a, B.Z, B.zlo, B.zstride, B.G, B.vlo, B.vstride);
+  if (a.curv_alpha > 0)
+    k_ngf_adj4<D, true><<<g2, 256, 0, L.stream>>>(a, B.Z, B.zlo, B.zstride, B.G, B.vlo, B.vstride);
+  else
+    k_ngf_adj4<D><<<g2, 256, 0, L.stream>>>(a, B.Z, B.zlo, B.zstride, B.G, B.vlo, B.vstride);
   return cudaGetLastError();
 }
 cudaError_t ngf_pass1_d2(const Launch& L, const Args& a, const NgfBufs& B, double* part, size_t cap, int* nblk);

@@ -307,16 +307,24 @@ class EvalPlan:
                                ctypes.c_void_p(out.data_ptr()), int(g_off), stride))
         return out
 
-    def evaluate(self, prob: SrProblem, weights, cell_volume: float, grad_out: torch.Tensor | None) -> torch.Tensor:
-        """Whole evaluation on one device; returns the device stats (D = stats[0])."""
+    def evaluate(self, prob: SrProblem, weights, cell_volume: float, grad_out: torch.Tensor | None,
+                 alpha: float = 0.0, s_out: torch.Tensor | None = None) -> torch.Tensor:
+        """Whole evaluation on one device; returns the device stats (D = stats[0]).  alpha > 0 adds the
+        curvature regulariser (sr_evaluate_reg): S in s_out[0], dS/dy added to grad_out."""
         w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64))
         if w.size != self.k:
             raise ValueError("one weight per subset frame required")
         self.engine.bind_stream()
-        check(self.lib.sr_evaluate(self.engine.ctx, ctypes.byref(prob), w.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
-                                   float(cell_volume), ctypes.c_void_p(self.raw.data_ptr()),
-                                   ctypes.c_void_p(self.stats.data_ptr()),
-                                   ctypes.c_void_p(grad_out.data_ptr() if grad_out is not None else 0)))
+        wp = w.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        gp = ctypes.c_void_p(grad_out.data_ptr() if grad_out is not None else 0)
+        if alpha > 0:
+            check(self.lib.sr_evaluate_reg(self.engine.ctx, ctypes.byref(prob), wp, float(cell_volume), float(alpha),
+                                           ctypes.c_void_p(self.raw.data_ptr()), ctypes.c_void_p(self.stats.data_ptr()),
+                                           gp, ctypes.c_void_p(s_out.data_ptr())))
+        else:
+            check(self.lib.sr_evaluate(self.engine.ctx, ctypes.byref(prob), wp, float(cell_volume),
+                                       ctypes.c_void_p(self.raw.data_ptr()), ctypes.c_void_p(self.stats.data_ptr()),
+                                       gp))
         return self.stats
 
     def curvature(self, prob: SrProblem, alpha: float, cell_volume: float, grad: torch.Tensor,

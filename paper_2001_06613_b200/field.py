@@ -69,9 +69,10 @@ class FieldObjective:
         prob = self.plan.problem(y=y)
         if want_grad and grad is None:
             grad = torch.empty_like(y)
-        stats = self.plan.evaluate(prob, self.weights, self.cell_volume, grad if want_grad else None)
-        if self.alpha > 0 and want_grad:
-            self.plan.curvature(prob, self.alpha, self.cell_volume, grad, self.s_reg)
+        if self.alpha > 0 and want_grad:  # one evaluation with the regulariser (sr_evaluate_reg)
+            stats = self.plan.evaluate(prob, self.weights, self.cell_volume, grad, self.alpha, self.s_reg)
+        else:
+            stats = self.plan.evaluate(prob, self.weights, self.cell_volume, grad if want_grad else None)
         return stats, grad
 
     def value(self, y: torch.Tensor) -> float:

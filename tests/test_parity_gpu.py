@@ -414,3 +414,34 @@ def test_single_frame_and_bad_args():
     with pytest.raises(NotImplementedError):
         srb.FieldObjective(fd, [0] * 129, np.ones(129), 1.0).evaluate(
             torch.zeros((129, 2, 64), dtype=torch.float64, device=fd.data.device))
+
+
+@pytest.mark.parametrize("dims", [(40, 24), (12, 10, 9)])
+def test_curvature_fused_ngf_pass2(dims):
+    """sr_evaluate_reg on the split fp32 NGF path adds alpha h L L (y - x) inside k_ngf_adj4: the gradient is
+    bitwise the unfused one (sr_evaluate then sr_curvature, the same float addition) and S agrees to 1e-12;
+    both match the oracle (D + S and dD/dy + dS/dy) at the fp32 tolerance."""
+    rng = np.random.default_rng(5)
+    frames, spacing, origin, y, w = _random_problem(rng, dims, 5, amp=0.3)
+    h = float(np.prod(spacing))
+    fd = _frames_dev(frames, dims, spacing, origin, torch.float32)
+    yt = torch.as_tensor(y).to(device=fd.data.device, dtype=torch.float32).contiguous()
+    obj = srb.FieldObjective(fd, list(range(5)), w, h, feature="ngf", ngf_eps=0.5, alpha=1.5)
+    stats, g = obj.evaluate(yt)
+    S = float(obj.s_reg.item())
+    D = float(stats[0].item())
+    plan = obj.plan
+    prob = plan.problem(y=yt)
+    g2 = torch.empty_like(yt)
+    s2 = torch.zeros(1, dtype=torch.float64, device=yt.device)
+    plan.evaluate(prob, w, h, g2)
+    plan.curvature(prob, 1.5, h, g2, s2)
+    assert torch.equal(g, g2)
+    assert S == pytest.approx(float(s2.item()), rel=1e-12)
+    q = frames.astype(np.float32).astype(np.float64)
+    yq = y.astype(np.float32).astype(np.float64)
+    _, Dref, gref = orc.evaluate_field(list(q), dims, spacing, origin, yq, w, h, "ngf", 0.5)
+    Sref, gS = orc.curvature(yq, dims, spacing, origin, 1.5, h)
+    assert D == pytest.approx(Dref, rel=1e-4)
+    assert S == pytest.approx(Sref, rel=1e-4)
+    assert _relmax(g.double().cpu().numpy(), gref + gS) < 1e-4
