@@ -21,6 +21,7 @@
  *                     parameters                                    (similarity.py:203-220, grid.py:246-253)
  *   sr_curvature      curvature regulariser S(y) and its gradient   (absent in the reference)
  *   sr_evaluate_reg   sr_evaluate + S(y) (fused into pass 2 on the split NGF path)
+ *   sr_sample         warped values T_j(y_j(x)) (CorrelationState.features; off the evaluation path)
  *   sr_ls_predict     temporal prolongation: smoothing least squares
  *                     with a shared tridiagonal matrix               (temporal.py:194-239, thomas_solve 166-191)
  *   sr_interp_linear  temporal prolongation at the coarsest level    (temporal.py:109-127)
@@ -194,6 +195,12 @@ SR_API int sr_evaluate_reg(sr_ctx* ctx, const sr_problem* prob, const double* we
  * [pix_lo, pix_hi) and writes this slab's S to s_out_dev[0] (one double). */
 SR_API int sr_curvature(sr_ctx* ctx, const sr_problem* prob, double alpha, double cell_volume,
                  void* grad_dev, int64_t g_off, int64_t g_stride, double* s_out_dev);
+
+/* The warped values T_j(y_j(x)) (affine rows or displacement fields, the sampling of grid.py:199-243)
+ * of every subset frame over [pix_lo, pix_hi): out_dev[j * (pix_hi - pix_lo) + (p - pix_lo)], in the
+ * problem's dtype.  Backs the lazily materialised CorrelationState.features (similarity.py:109-125);
+ * not on the evaluation path. */
+SR_API int sr_sample(sr_ctx* ctx, const sr_problem* prob, void* out_dev);
 
 /* Temporal prolongation for fields of m components per frame (temporal.py:194-239):
  * solves (Mask + beta*Lap) zeta = Mask*eta + beta*Lap*ref for every component.

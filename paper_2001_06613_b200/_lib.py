@@ -139,6 +139,7 @@ EXPORTS = {
     "sr_grad": (_c.c_int, [_P, _PROB, _P, _P, _c.c_int64, _c.c_int64]),
     "sr_evaluate": (_c.c_int, [_P, _PROB, _D, _c.c_double, _P, _P, _P]),
     "sr_evaluate_reg": (_c.c_int, [_P, _PROB, _D, _c.c_double, _c.c_double, _P, _P, _P, _P]),
+    "sr_sample": (_c.c_int, [_P, _PROB, _P]),
     "sr_curvature": (
         _c.c_int,
         [_P, _PROB, _c.c_double, _c.c_double, _P, _c.c_int64, _c.c_int64, _P],

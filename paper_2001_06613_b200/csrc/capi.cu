@@ -1003,6 +1003,18 @@ static int curvature_impl(sr_ctx* c, const sr_problem* p, double alpha, double h
   return SR_OK;
 }
 
+int sr_sample(sr_ctx* c, const sr_problem* p, void* out_dev) {
+  int rc = check_problem(c, p);
+  if (rc) return rc;
+  if (!out_dev) return fail(SR_ERR_ARG, "null out");
+  CK(cudaSetDevice(c->device));
+  rc = upload_job(c, p, nullptr);
+  if (rc) return rc;
+  Args a = make_args(c, p);
+  CK(SR_SWITCH(p->dtype, p->grid.ndim, sample, p->param, launch_of(c), a, out_dev));
+  return SR_OK;
+}
+
 int sr_ls_predict(sr_ctx* c, int32_t dtype, int32_t n, int64_t m, const uint8_t* mask, double beta,
                   const void* eta, const void* ref, void* zeta) {
   if (!c || !mask || !eta || !ref || !zeta) return fail(SR_ERR_ARG, "null argument");

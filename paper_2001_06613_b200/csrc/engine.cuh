@@ -1237,6 +1237,24 @@ __device__ __forceinline__ double lap_u(const Args& a, const T* __restrict__ yc,
   return out;
 }
 
+// T_j(y_j(x)) for every subset frame j and pixel of [pix_lo, pix_hi): out[j][pix - pix_lo] (sr_sample; the
+// warped values behind CorrelationState.features, similarity.py:143-150)
+template <typename T, int D, int PARAM>
+__global__ void __launch_bounds__(256) k_sample_values(const Args a, T* __restrict__ out) {
+  const int j = blockIdx.y;
+  const long long pix = a.pix_lo + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pix >= a.pix_hi) return;
+  int c[3];
+  coords<D>(a.g, pix, c);
+  const T* img = reinterpret_cast<const T*>(a.frames) + (long long)a.job->frame_index[j] * a.g.N;
+  using P = typename std::conditional<PARAM == AFFINE, double, T>::type;
+  P p[D];
+  warp_point<T, P, D, PARAM>(a, j, pix, c, p);
+  T gr[D];
+  const T v = a.g.pow2 ? interp<T, P, D, false, true>(img, a.g, p, gr) : interp<T, P, D, false, false>(img, a.g, p, gr);
+  out[(long long)j * (a.pix_hi - a.pix_lo) + (pix - a.pix_lo)] = v;
+}
+
 // alpha h (L L u)(pix) for u = y - x of one component (the arithmetic of k_curvature); adds this
 // pixel's 1/2 alpha h (L u)^2 to *sval
 template <typename T, int D>

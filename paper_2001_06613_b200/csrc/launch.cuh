@@ -468,6 +468,14 @@ struct Dispatch {
                                size_t cap, int* nb) {
     return run_curvature<T, D>(L, a, alpha, h, part, cap, nb);
   }
+  static cudaError_t sample(int param, const Launch& L, const Args& a, void* out) {
+    const long long npix = a.pix_hi - a.pix_lo;
+    if (npix <= 0) return cudaSuccess;
+    const dim3 grid((unsigned)((npix + 255) / 256), (unsigned)a.K);
+    if (param == AFFINE) k_sample_values<T, D, AFFINE><<<grid, 256, 0, L.stream>>>(a, reinterpret_cast<T*>(out));
+    else k_sample_values<T, D, DISP><<<grid, 256, 0, L.stream>>>(a, reinterpret_cast<T*>(out));
+    return cudaGetLastError();
+  }
 };
 
 // Entry points implemented in inst_<dtype>_d<D>.cu
@@ -479,7 +487,8 @@ struct Dispatch {
   cudaError_t adjoint_##TT##_d##DD(int param, const Launch& L, const Args& a, const void* zb, \
                                    long long zo, long long zs, double* pa, size_t cap, int* nb); \
   cudaError_t curvature_##TT##_d##DD(const Launch& L, const Args& a, double alpha, double h,  \
-                                     double* part, size_t cap, int* nb);
+                                     double* part, size_t cap, int* nb);                     \
+  cudaError_t sample_##TT##_d##DD(int param, const Launch& L, const Args& a, void* out);
 
 #define SR_DEFINE_INST(TT, T, DD)                                                             \
   cudaError_t pass1_##TT##_d##DD(int feat, int param, int KP, const Launch& L, const Args& a, \
@@ -497,6 +506,9 @@ struct Dispatch {
   cudaError_t curvature_##TT##_d##DD(const Launch& L, const Args& a, double alpha, double h,  \
                                      double* part, size_t cap, int* nb) {                     \
     return Dispatch<T, DD>::curvature(L, a, alpha, h, part, cap, nb);                         \
+  }                                                                                           \
+  cudaError_t sample_##TT##_d##DD(int param, const Launch& L, const Args& a, void* out) {     \
+    return Dispatch<T, DD>::sample(param, L, a, out);                                         \
   }
 
 SR_DECLARE_INST(f32, 2)

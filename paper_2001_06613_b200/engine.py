@@ -284,6 +284,14 @@ class EvalPlan:
         return p
 
     # ---------------------------------------------------------------- the passes
+    def sample(self, prob: SrProblem) -> torch.Tensor:
+        """The warped values T_j(y_j(x)) of the problem's slab, [k, pix_hi - pix_lo] (sr_sample)."""
+        out = torch.empty((self.k, int(prob.pix_hi - prob.pix_lo)), dtype=self.frames.dtype,
+                          device=self.frames.data.device)
+        self.engine.bind_stream()
+        check(self.lib.sr_sample(self.engine.ctx, ctypes.byref(prob), ctypes.c_void_p(out.data_ptr())))
+        return out
+
     def corr_partial(self, prob: SrProblem) -> torch.Tensor:
         self.engine.bind_stream()
         check(self.lib.sr_corr_partial(self.engine.ctx, ctypes.byref(prob), ctypes.c_void_p(self.raw.data_ptr())))

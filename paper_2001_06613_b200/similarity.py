@@ -83,8 +83,12 @@ class CorrelationState:
     """Mirror of similarity.py:109-125.
 
     ``corr``, ``degenerate``, ``center_norms`` and ``weights`` are host arrays
-    like the reference's.  The N x K feature matrix is never materialised: the
-    gradient pass re-warps the frames on the device instead.
+    like the reference's.  The evaluation never materialises the N x K feature
+    matrix (the gradient pass re-warps the frames on the device, DESIGN.md §3);
+    ``features`` builds it on first access only: the device re-samples the warped
+    values (sr_sample) and forms the reference's feature columns (similarity.py:73-87:
+    centred, unit norm, zero for a degenerate frame; NGF: n / ||n|| over the d
+    component images), returned as a host N x K (NGF: dN x K) array.
     """
 
     subset: tuple
@@ -95,13 +99,45 @@ class CorrelationState:
     center_norms: np.ndarray
     means: np.ndarray = field(default=None, repr=False)
     _plan: EvalPlan = field(default=None, repr=False, compare=False)
+    _prob: object = field(default=None, repr=False, compare=False)
+    _prob_keep: object = field(default=None, repr=False, compare=False)  # the host affine rows _prob points at
+    _features: np.ndarray = field(default=None, repr=False, compare=False)
 
     @property
-    def features(self):
-        raise AttributeError(
-            "features are virtual on the B200 engine (never stored in HBM); "
-            "use corr / center_norms, or the reference implementation for the N x K matrix"
-        )
+    def features(self) -> np.ndarray:
+        if self._features is None:
+            if self._plan is None or self._prob is None:
+                raise AttributeError("this state holds no device plan to materialise the features from")
+            self._features = _materialise_features(self._plan, self._prob, self.degenerate)
+        return self._features
+
+
+def _materialise_features(plan: EvalPlan, prob, degenerate) -> np.ndarray:
+    v = plan.sample(prob).to(torch.float64)  # [k, N]
+    if plan.feature == "ngf":
+        g = plan.grid
+        u = v.reshape((v.shape[0],) + tuple(reversed(g.dims)))  # [k, n_{d-1}, ..., n_0] (first axis fastest)
+        comps = []
+        for ax in range(g.ndim):
+            dim = u.dim() - 1 - ax
+            n = u.shape[dim]
+            up = torch.cat([u.narrow(dim, 1, n - 1), u.narrow(dim, n - 1, 1)], dim)
+            um = torch.cat([u.narrow(dim, 0, 1), u.narrow(dim, 0, n - 1)], dim)
+            scale = torch.full((n,), 0.5 / g.spacing[ax], dtype=torch.float64, device=u.device)
+            scale[0] = scale[-1] = 1.0 / g.spacing[ax]  # one-sided at the domain edge
+            shape = [1] * u.dim()
+            shape[dim] = n
+            comps.append((up - um) * scale.reshape(shape))
+        p = torch.stack([c.reshape(v.shape[0], -1) for c in comps], dim=1)  # [k, d, N]
+        nvec = p / torch.sqrt((p * p).sum(dim=1, keepdim=True) + plan.ngf_eps ** 2)
+        f = nvec.reshape(v.shape[0], -1)
+    else:
+        f = v - v.mean(dim=1, keepdim=True)
+    norms = torch.linalg.vector_norm(f, dim=1, keepdim=True)
+    f = torch.where(norms > 0, f / torch.where(norms > 0, norms, 1.0), torch.zeros_like(f))
+    deg = torch.as_tensor(np.asarray(degenerate, dtype=bool), device=f.device)
+    f[deg] = 0.0
+    return f.T.contiguous().cpu().numpy()
 
 
 def correlation_state(seq, stack, subset, weights, cell_volume: float, threads: int = 1) -> CorrelationState:
@@ -128,6 +164,8 @@ def correlation_state(seq, stack, subset, weights, cell_volume: float, threads: 
         center_norms=st["sigma"],
         means=st["mean"],
         _plan=plan,
+        _prob=prob,
+        _prob_keep=getattr(plan, "_affine_buf", None),
     )
 
 

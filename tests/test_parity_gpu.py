@@ -445,3 +445,21 @@ def test_curvature_fused_ngf_pass2(dims):
     assert D == pytest.approx(Dref, rel=1e-4)
     assert S == pytest.approx(Sref, rel=1e-4)
     assert _relmax(g.double().cpu().numpy(), gref + gS) < 1e-4
+
+
+@pytest.mark.parametrize("name", ["aff2d_small_0", "aff2d_subset_outside", "aff3d_small", "aff2d_degenerate"])
+def test_lazy_features_match_reference(name, golden):
+    """CorrelationState.features (similarity.py:109-125) materialised on first access from the device's warped
+    values: equal to the reference's own feature matrix (run here from baseline/_ref) to 1e-12, zero columns for
+    degenerate frames, and features^T features == corr."""
+    from seqreg import similarity as ref_sim
+
+    case = golden[name]
+    seq, stack, subset = _seq_stack(case)
+    st = srb.correlation_state(seq, stack, subset, case["weights"], float(case["h"]))
+    ref = ref_sim.correlation_state(seq, stack, subset, case["weights"], float(case["h"]))
+    f = st.features
+    assert f.shape == ref.features.shape
+    np.testing.assert_allclose(f, ref.features, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(f.T @ f, st.corr, rtol=0, atol=1e-12)
+    assert st.features is f  # materialised once
