@@ -76,6 +76,8 @@ def exchange_halo(y_local: torch.Tensor, dims, lo: int, hi: int, halo_rows: int,
     world = dist.get_world_size(group)
     row = int(np.prod(dims[:-1]))
     ylo, yhi = halo_range(dims, lo, hi, halo_rows)
+    # NCCL moves device buffers directly; gloo's point-to-point needs host memory (CPU tests, gloo runs)
+    stage = y_local.is_cuda and dist.get_backend(group) == "gloo"
     ops = []
     bufs = []
     # my first/last owned rows go to the neighbours' halos; their rows fill mine
@@ -83,18 +85,23 @@ def exchange_halo(y_local: torch.Tensor, dims, lo: int, hi: int, halo_rows: int,
         n = min(halo_rows * row, hi - lo)
         send = y_local[..., lo - ylo:lo - ylo + n].contiguous()
         recv = torch.empty_like(y_local[..., :lo - ylo])
+        if stage:
+            send, recv = send.cpu(), recv.cpu()
         ops += [dist.P2POp(dist.isend, send, rank - 1, group), dist.P2POp(dist.irecv, recv, rank - 1, group)]
         bufs.append(("lo", recv))
     if rank < world - 1:
         n = min(halo_rows * row, hi - lo)
         send = y_local[..., hi - ylo - n:hi - ylo].contiguous()
         recv = torch.empty_like(y_local[..., hi - ylo:])
+        if stage:
+            send, recv = send.cpu(), recv.cpu()
         ops += [dist.P2POp(dist.isend, send, rank + 1, group), dist.P2POp(dist.irecv, recv, rank + 1, group)]
         bufs.append(("hi", recv))
     if ops:
         for r in dist.batch_isend_irecv(ops):
             r.wait()
     for side, buf in bufs:
+        buf = buf.to(y_local.device)
         if side == "lo":
             y_local[..., :lo - ylo] = buf
         else:
