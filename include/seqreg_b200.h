@@ -132,7 +132,10 @@ SR_API const char* sr_status_string(int status);
 
 SR_API int sr_create(int32_t device, sr_ctx** out);
 SR_API int sr_destroy(sr_ctx* ctx);
-/* Use this cudaStream_t (NULL = legacy default stream) for every later call. */
+/* Use this cudaStream_t (NULL = legacy default stream) for every later call.  A context's calls are
+ * ordered: on a change of stream the new stream first waits (device-side event) for the work already
+ * queued on the previous one, because a context's scratch buffers are shared by all its calls.  Use one
+ * context per concurrent stream for overlapping evaluations. */
 SR_API int sr_set_stream(sr_ctx* ctx, void* stream);
 /* Number of CTAs the persistent kernels launch (defaults to a multiple of the SM count). */
 SR_API int sr_set_grid_ctas(sr_ctx* ctx, int32_t ctas);

@@ -90,6 +90,7 @@ struct sr_ctx {
   double* part = nullptr;
   size_t part_cap = 0;  // doubles
   unsigned* ticket = nullptr;  // last-block ticket of k_reduce_finalize
+  cudaEvent_t order_ev = nullptr;  // orders calls across a change of stream (sr_set_stream)
   sr::lbfgs::Workspace* lbfgs = nullptr;  // device L-BFGS vectors (lbfgs.cu)
   void* zbuf = nullptr;
   size_t zbuf_bytes = 0;
@@ -565,6 +566,7 @@ int sr_destroy(sr_ctx* c) {
   cudaFree(c->part);
   cudaFree(c->ticket);
   cudaFree(c->curv_part);
+  if (c->order_ev) cudaEventDestroy(c->order_ev);
   sr::lbfgs::destroy(c->lbfgs);
   cudaFree(c->vbuf);
   cudaFree(c->gbuf);
@@ -582,9 +584,23 @@ int sr_destroy(sr_ctx* c) {
   return SR_OK;
 }
 
+// A context's scratch (job constants, partials, tickets, split-path buffers) is shared by every call, so
+// calls issued from different streams must not overlap: when the stream changes, the new stream waits
+// for everything already queued on the previous one (an event, no host synchronisation).
 int sr_set_stream(sr_ctx* c, void* stream) {
   if (!c) return fail(SR_ERR_ARG, "null context");
-  c->stream = (cudaStream_t)stream;
+  const cudaStream_t ns = (cudaStream_t)stream;
+  if (ns != c->stream) {
+    cudaStreamCaptureStatus a = cudaStreamCaptureStatusNone, b = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(c->stream, &a));
+    CK(cudaStreamIsCapturing(ns, &b));
+    if (a == cudaStreamCaptureStatusNone && b == cudaStreamCaptureStatusNone) {
+      if (!c->order_ev) CK(cudaEventCreateWithFlags(&c->order_ev, cudaEventDisableTiming));
+      CK(cudaEventRecord(c->order_ev, c->stream));
+      CK(cudaStreamWaitEvent(ns, c->order_ev, 0));
+    }
+    c->stream = ns;
+  }
   return SR_OK;
 }
 

@@ -463,3 +463,26 @@ def test_lazy_features_match_reference(name, golden):
     np.testing.assert_allclose(f, ref.features, rtol=0, atol=1e-12)
     np.testing.assert_allclose(f.T @ f, st.corr, rtol=0, atol=1e-12)
     assert st.features is f  # materialised once
+
+
+def test_context_orders_calls_across_streams():
+    """Evaluations issued on alternating torch streams against one context (shared scratch) give the
+    same D and gradient as on one stream: sr_set_stream makes the new stream wait for the old one."""
+    rng = np.random.default_rng(9)
+    dims = (96, 80)
+    frames, spacing, origin, y, w = _random_problem(rng, dims, 12, amp=0.3)
+    fd = _frames_dev(frames, dims, spacing, origin, torch.float32)
+    obj = srb.FieldObjective(fd, list(range(12)), w, float(np.prod(spacing)))
+    yt = torch.as_tensor(y).to(device=fd.data.device, dtype=torch.float32).contiguous()
+    stats, g = obj.evaluate(yt)
+    D0, g0 = float(stats[0].item()), g.clone()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = []
+    for i in range(6):
+        with torch.cuda.stream(streams[i % 2]):
+            st, gi = obj.evaluate(yt, torch.empty_like(yt))
+            outs.append((st[0].clone(), gi))
+    torch.cuda.synchronize()
+    for d, gi in outs:
+        assert float(d.item()) == D0
+        assert torch.equal(gi, g0)
