@@ -285,12 +285,16 @@ struct TGX {
   // R tiles accumulate in a TMEM slot (fp32, 512 columns) between fp64 flushes: the flush of a
   // 128 x N slot, not the MMAs, bounds this kernel (R = 4 -> 16 at KP = 128: 0.71 -> 0.45 ms at C3)
   static constexpr int NST = 2, NB = 2, NA = 2, R = KP == 64 ? 8 : 16;
-  static constexpr int N = KP;                   // MMA N and TMEM columns per slot
+  // KP = 128: one MMA per K8 step, A = H (rows 0..127 of the [H (KPN rows); L (KPN rows)] buffer), B = the
+  // whole buffer (N = 2 KPN, KPN = K rounded up to 16): D = [H H^T | H L^T]; the flush accumulates
+  // 0.5 HH + HL in fp64 and G = A + A^T at the end (= HH + HL + LH).  (0.58x the tensor work of the
+  // three N = 128 MMAs hi.hi + lo.hi + hi.lo.)
+  static constexpr int N = KP == 128 ? 256 : KP;  // TMEM columns per slot (MMA N = 2 KPN <= 256 at KP = 128)
   static constexpr int SBYTES = KP * TP * 4;     // fp32 stage [KP][32]
-  static constexpr int OBYTES = 128 * TP * 4;    // one 128-row operand tile (TP / 32 column atoms of 16 KB)
-  static constexpr int NOPS = KP == 128 ? 2 : 1; // operand tiles per buffer (hi, lo) or ([hi; lo])
-  static constexpr uint32_t IDESC = umma_idesc_tf32(128, N);
-  static constexpr int ACC_ROWS = 128, ACC_COLS = N;
+  static constexpr int OBYTES = (KP == 128 ? 256 : 128) * TP * 4;  // [H; L] rows x TP columns (KP = 64: [hi; lo])
+  static constexpr int NOPS = 1;
+  static constexpr uint32_t IDESC = umma_idesc_tf32(128, KP);  // KP = 64 (KP = 128 uses the runtime N = 2 KPN)
+  static constexpr int ACC_ROWS = 128, ACC_COLS = KP == 128 ? 128 : N;
 };
 
 template <int KP>
@@ -341,7 +345,9 @@ __global__ void __launch_bounds__(TGX<KP>::NT, 1) k_gram_tcx(const Args a, const
     tma_prefetch_desc(&xmap);
   }
   for (int e = tid; e < C::ACC_ROWS * NC; e += C::NT) accs[e] = 0.0;
-  if (warp == C::NSP / 32) tmem_alloc(tmem_slot, NC * NA);
+  const int KPN = KP == 128 ? (K + 15) / 16 * 16 : KP;  // rows of H (and of L) in the KP = 128 buffer
+  constexpr int TS = C::N;                              // TMEM columns per slot
+  if (warp == C::NSP / 32) tmem_alloc(tmem_slot, TS * NA);
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
@@ -375,14 +381,15 @@ __global__ void __launch_bounds__(TGX<KP>::NT, 1) k_gram_tcx(const Args a, const
           lo[u] = qv[u] - hi[u];
         }
         const int col = part * CPT + 4 * h;
-        const int atom = col >> 5, g = (col & 31) >> 2;  // 128-row column atom (16 KB), 16-byte chunk
-        const int rh = r, rl = KP == 128 ? r : 64 + r;
-        unsigned char* hb = ob + atom * (128 * 128);
-        unsigned char* lb = (KP == 128 ? ob + C::OBYTES : ob) + atom * (128 * 128);
-        *reinterpret_cast<float4*>(hb + (rh >> 3) * 1024 + (rh & 7) * 128 + (((g ^ (rh & 7)) & 7) << 4)) =
-            make_float4(hi[0], hi[1], hi[2], hi[3]);
-        *reinterpret_cast<float4*>(lb + (rl >> 3) * 1024 + (rl & 7) * 128 + (((g ^ (rl & 7)) & 7) << 4)) =
-            make_float4(lo[0], lo[1], lo[2], lo[3]);
+        const int atom = col >> 5, g = (col & 31) >> 2;  // column atom (TP = 32 at KP = 128), 16-byte chunk
+        const int rh = r, rl = KP == 128 ? KPN + r : 64 + r;
+        if (KP != 128 || r < KPN) {
+          unsigned char* hb = ob + atom * (128 * 128);
+          *reinterpret_cast<float4*>(hb + (rh >> 3) * 1024 + (rh & 7) * 128 + (((g ^ (rh & 7)) & 7) << 4)) =
+              make_float4(hi[0], hi[1], hi[2], hi[3]);
+          *reinterpret_cast<float4*>(hb + (rl >> 3) * 1024 + (rl & 7) * 128 + (((g ^ (rl & 7)) & 7) << 4)) =
+              make_float4(lo[0], lo[1], lo[2], lo[3]);
+        }
       }
       fence_proxy_async_smem();
       mbar_arrive(&vb_full[b]);  // also releases stage st
@@ -407,20 +414,16 @@ __global__ void __launch_bounds__(TGX<KP>::NT, 1) k_gram_tcx(const Args a, const
         if (first && grp >= NA) mbar_wait(&acc_free[s], (uint32_t)((grp / NA - 1) & 1));
         tc_fence_after();
         const uint32_t o0 = smem_u32(Vb + (size_t)b * C::NOPS * C::OBYTES);
-        const uint32_t acc = tmem + (uint32_t)(s * NC);
+        const uint32_t acc = tmem + (uint32_t)(s * TS);
+        const uint32_t idesc = KP == 128 ? umma_idesc_tf32(128, 2 * KPN) : C::IDESC;
 #pragma unroll
         for (int k8 = 0; k8 < TP / 8; ++k8) {
           const uint32_t acc_in = (k8 > 0 || !first) ? 1u : 0u;
           const uint32_t koff = (uint32_t)((k8 >> 2) * (128 * 128) + (k8 & 3) * 32);
           const uint64_t dh = umma_sdesc_sw128(o0 + koff);
-          if (KP == 128) {
-            const uint64_t dl = umma_sdesc_sw128(o0 + C::OBYTES + koff);
-            umma_tf32(acc, dh, dh, C::IDESC, acc_in);
-            umma_tf32(acc, dl, dh, C::IDESC, 1u);
-            umma_tf32(acc, dh, dl, C::IDESC, 1u);
-          } else {
-            umma_tf32(acc, dh, dh, C::IDESC, acc_in);  // A = [hi; lo] (128 rows), B = hi (first 64 rows)
-          }
+          // KP = 128: A = H (128 rows from the buffer start), B = [H; L] (2 KPN rows); KP = 64: A = [hi; lo]
+          // (128 rows), B = hi (first 64 rows)
+          umma_tf32(acc, dh, dh, idesc, acc_in);
         }
         umma_commit(&vb_free[b]);
         if (last) umma_commit(&acc_full[s]);
@@ -436,12 +439,32 @@ __global__ void __launch_bounds__(TGX<KP>::NT, 1) k_gram_tcx(const Args a, const
       const int s = (int)(n % NA);
       mbar_wait(&acc_full[s], (uint32_t)((n / NA) & 1));
       tc_fence_after();
+      const uint32_t ts = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(s * TS);
+      if (KP == 128) {  // 0.5 HH + HL, 32 (last: 16) columns at a time
 #pragma unroll 1
-      for (int ch = 0; ch < NC / 32; ++ch) {
-        float v[32];
-        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(s * NC + ch * 32), v);
+        for (int c0 = 0; c0 < KPN; c0 += 32) {
+          if (c0 + 32 <= KPN) {
+            float hh[32], hl[32];
+            tmem_ld32(ts + (uint32_t)c0, hh);
+            tmem_ld32(ts + (uint32_t)(KPN + c0), hl);
 #pragma unroll
-        for (int cc = 0; cc < 32; ++cc) arow[(32 * ch + cc) ^ lane] += (double)v[cc];
+            for (int cc = 0; cc < 32; ++cc) arow[(c0 + cc) ^ lane] += 0.5 * (double)hh[cc] + (double)hl[cc];
+          } else {
+            float hh[16], hl[16];
+            tmem_ld16(ts + (uint32_t)c0, hh);
+            tmem_ld16(ts + (uint32_t)(KPN + c0), hl);
+#pragma unroll
+            for (int cc = 0; cc < 16; ++cc) arow[(c0 + cc) ^ lane] += 0.5 * (double)hh[cc] + (double)hl[cc];
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int ch = 0; ch < NC / 32; ++ch) {
+          float v[32];
+          tmem_ld32(ts + (uint32_t)(ch * 32), v);
+#pragma unroll
+          for (int cc = 0; cc < 32; ++cc) arow[(32 * ch + cc) ^ lane] += (double)v[cc];
+        }
       }
       tc_fence_before();
       mbar_arrive(&acc_free[s]);
@@ -453,11 +476,11 @@ __global__ void __launch_bounds__(TGX<KP>::NT, 1) k_gram_tcx(const Args a, const
     auto A = [&](int i, int j) { return accs[(size_t)i * NC + (j ^ (i & 31))]; };
     for (int e = tid - (C::NSP + 32); e < KP * KP; e += 128) {
       const int i = e / KP, j = e % KP;
-      out[e] = KP == 128 ? A(i, j) : A(i, j) + A(64 + i, j) + A(64 + j, i);
+      out[e] = KP == 128 ? (i < KPN && j < KPN ? A(i, j) + A(j, i) : 0.0) : A(i, j) + A(64 + i, j) + A(64 + j, i);
     }
   } else if (warp == C::NSP / 32) {
     tc_fence_after();
-    tmem_dealloc(tmem, NC * NA);
+    tmem_dealloc(tmem, TS * NA);
   }
 }
 
@@ -501,16 +524,41 @@ __device__ __forceinline__ double finish2(const Corners2& c, const Geo& g, bool 
   return c.inside ? fma((double)c.f1, a1 - a0, a0) : 0.0;
 }
 
-template <bool POW2>
-__global__ void __launch_bounds__(256, 2) k_ngf_sfeat2(const Args a, int seg, int rz0, int rz1, int rs0, int rs1,
-                                                       float* __restrict__ Nf, float* __restrict__ IRho,
-                                                       long long zlo, long long zstride, float* __restrict__ Gv,
-                                                       long long vlo, long long vstride) {
+// PX consecutive columns per thread (2: 512 threads for a 1024-pixel row, 32 warps per SM at <= 64
+// registers; 4 held 128 registers and 16 warps)
+template <int PX>
+struct VecF;
+template <>
+struct VecF<2> {
+  using T = float2;
+  static __device__ __forceinline__ void ld(const float* p, float (&v)[2]) {
+    const float2 a = __ldg(reinterpret_cast<const float2*>(p));
+    v[0] = a.x, v[1] = a.y;
+  }
+  static __device__ __forceinline__ void st(float* p, const float (&v)[2]) {
+    *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+  }
+};
+template <>
+struct VecF<4> {
+  static __device__ __forceinline__ void ld(const float* p, float (&v)[4]) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+    v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w;
+  }
+  static __device__ __forceinline__ void st(float* p, const float (&v)[4]) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  }
+};
+
+template <bool POW2, int PX>
+__global__ void __launch_bounds__(1024 / (4 / PX) <= 512 ? 512 : 256, 2) k_ngf_sfeat2(
+    const Args a, int seg, int rz0, int rz1, int rs0, int rs1, float* __restrict__ Nf, float* __restrict__ IRho,
+    long long zlo, long long zstride, float* __restrict__ Gv, long long vlo, long long vstride) {
   __shared__ double edge[2][2][32];  // [row parity][left / right edge][warp]
   const int k = blockIdx.y;
   const int n0 = a.g.n[0], n1 = a.g.n[1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  const int x0 = 4 * tid;
+  const int x0 = PX * tid;
   const bool colok = x0 < n0;
   const int ra = rz0 + blockIdx.x * seg, rb = min(ra + seg, rz1);
   if (ra >= rb) return;
@@ -518,57 +566,66 @@ __global__ void __launch_bounds__(256, 2) k_ngf_sfeat2(const Args a, int seg, in
   const float* img = reinterpret_cast<const float*>(a.frames) + (long long)fi * a.g.N;
   const float* y0p = reinterpret_cast<const float*>(a.y) + (long long)(2 * k) * a.y_stride - a.y_off;
   const float* y1p = y0p + a.y_stride;
-  const bool vec = (n0 & 3) == 0 && ((a.y_stride | a.y_off) & 3) == 0 &&
-                   (reinterpret_cast<uintptr_t>(a.y) & 15) == 0 && x0 + 4 <= n0;
-  const bool vz = vec && ((zlo | zstride) & 3) == 0, vg = vec && ((vlo | vstride) & 3) == 0;
+  const bool vec = (n0 % PX) == 0 && ((a.y_stride | a.y_off) % PX) == 0 &&
+                   (reinterpret_cast<uintptr_t>(a.y) & (4 * PX - 1)) == 0 && x0 + PX <= n0;
+  const bool vz = vec && (zlo % PX) == 0 && (zstride % PX) == 0, vg = vec && (vlo % PX) == 0 && (vstride % PX) == 0;
   const double h0 = 0.5 * a.g.inv[0], f0 = a.g.inv[0], h1 = 0.5 * a.g.inv[1], f1 = a.g.inv[1];
   const float e = (float)a.eps, e2 = e * e;
   float* gk0 = Gv + (long long)(2 * k) * vstride - vlo;
   float* gk1 = gk0 + vstride;
-  auto load_y = [&](int r, float (&py)[4][2]) {
+  auto load_y = [&](int r, float (&py)[PX][2]) {
     const long long pr = (long long)r * n0 + x0;
     if (colok && vec) {
-      const float4 a0 = __ldg(reinterpret_cast<const float4*>(y0p + pr));
-      const float4 a1 = __ldg(reinterpret_cast<const float4*>(y1p + pr));
-      py[0][0] = a0.x, py[1][0] = a0.y, py[2][0] = a0.z, py[3][0] = a0.w;
-      py[0][1] = a1.x, py[1][1] = a1.y, py[2][1] = a1.z, py[3][1] = a1.w;
+      float a0[PX], a1[PX];
+      VecF<PX>::ld(y0p + pr, a0);
+      VecF<PX>::ld(y1p + pr, a1);
+#pragma unroll
+      for (int t = 0; t < PX; ++t) py[t][0] = a0[t], py[t][1] = a1[t];
     } else {
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
+      for (int t = 0; t < PX; ++t) {
         const bool ok = colok && x0 + t < n0;
         py[t][0] = ok ? __ldg(y0p + pr + t) : 0.f;
         py[t][1] = ok ? __ldg(y1p + pr + t) : 0.f;
       }
     }
   };
-  auto fetch_row = [&](const float (&py)[4][2], Corners2 (&cr)[4]) {
+  auto fetch_row = [&](const float (&py)[PX][2], Corners2 (&cr)[PX]) {
 #pragma unroll
-    for (int t = 0; t < 4; ++t) cr[t] = fetch2<POW2>(img, a.g, py[t][0], py[t][1]);
+    for (int t = 0; t < PX; ++t) cr[t] = fetch2<POW2>(img, a.g, py[t][0], py[t][1]);
   };
   // u of row r from its corners; grad T written when r is a slab row of this segment
-  auto finish_row = [&](int r, const Corners2 (&cr)[4], double (&u)[4]) {
-    float gt[4][2];
+  auto finish_row = [&](int r, const Corners2 (&cr)[PX], double (&u)[PX]) {
+    float gt0[PX], gt1[PX];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) u[t] = finish2(cr[t], a.g, POW2, gt[t]);
+    for (int t = 0; t < PX; ++t) {
+      float gt[2];
+      u[t] = finish2(cr[t], a.g, POW2, gt);
+      gt0[t] = gt[0], gt1[t] = gt[1];
+    }
     if (colok && r >= ra && r < rb && r >= rs0 && r < rs1) {
       const long long q = (long long)r * n0 + x0;
       if (vg) {
-        *reinterpret_cast<float4*>(gk0 + q) = make_float4(gt[0][0], gt[1][0], gt[2][0], gt[3][0]);
-        *reinterpret_cast<float4*>(gk1 + q) = make_float4(gt[0][1], gt[1][1], gt[2][1], gt[3][1]);
+        VecF<PX>::st(gk0 + q, gt0);
+        VecF<PX>::st(gk1 + q, gt1);
       } else {
 #pragma unroll
-        for (int t = 0; t < 4; ++t)
+        for (int t = 0; t < PX; ++t)
           if (x0 + t < n0) {
-            gk0[q + t] = gt[t][0];
-            gk1[q + t] = gt[t][1];
+            gk0[q + t] = gt0[t];
+            gk1[q + t] = gt1[t];
           }
       }
     }
   };
-  // prologue: u of rows ra - 1, ra, ra + 1 in registers, corners of ra + 2 and y of ra + 3 in flight
-  double um[4] = {0, 0, 0, 0}, uc[4], up[4] = {0, 0, 0, 0};
-  float yv[4][2];
-  Corners2 cr[4];
+  // prologue: u of rows ra - 1, ra, ra + 1 in registers; corners of ra + 2 landing, y of ra + 3 in flight.
+  // In iteration r the corners of row r + 3 and the y of row r + 4 are issued, row r + 2's corners (issued
+  // one iteration earlier) are finished at its end: every load has a whole row of work to land.
+  double um[PX], uc[PX], up[PX];
+#pragma unroll
+  for (int t = 0; t < PX; ++t) um[t] = up[t] = 0.0;
+  float yv[PX][2];
+  Corners2 cr[PX], cn[PX];
   if (ra > 0) {
     load_y(ra - 1, yv);
     fetch_row(yv, cr);
@@ -583,24 +640,28 @@ __global__ void __launch_bounds__(256, 2) k_ngf_sfeat2(const Args a, int seg, in
     finish_row(ra + 1, cr, up);
   }
   const int rlast = min(rb, n1 - 1);  // last row ever sampled by this segment
-  if (ra + 2 <= rlast) load_y(ra + 2, yv);
+  if (ra + 2 <= rlast) {
+    load_y(ra + 2, yv);
+    fetch_row(yv, cr);
+  }
+  if (ra + 3 <= rlast) load_y(ra + 3, yv);
   for (int r = ra; r < rb; ++r) {
     const int par = r & 1;
     const bool more = r + 2 <= rlast;
-    if (more) fetch_row(yv, cr);                  // corners of row r + 2 (in flight during row r)
-    if (r + 3 <= rlast) load_y(r + 3, yv);        // y of row r + 3
+    if (r + 3 <= rlast) fetch_row(yv, cn);        // corners of row r + 3 (finished next iteration)
+    if (r + 4 <= rlast) load_y(r + 4, yv);        // y of row r + 4
     if (lane == 0) edge[par][1][warp] = uc[0];
-    if (lane == 31) edge[par][0][warp] = uc[3];
+    if (lane == 31) edge[par][0][warp] = uc[PX - 1];
     __syncthreads();
-    double left = __shfl_up_sync(0xffffffffu, uc[3], 1), right = __shfl_down_sync(0xffffffffu, uc[0], 1);
+    double left = __shfl_up_sync(0xffffffffu, uc[PX - 1], 1), right = __shfl_down_sync(0xffffffffu, uc[0], 1);
     if (lane == 0) left = warp > 0 ? edge[par][0][warp - 1] : uc[0];
-    if (lane == 31) right = warp + 1 < nw ? edge[par][1][warp + 1] : uc[3];
+    if (lane == 31) right = warp + 1 < nw ? edge[par][1][warp + 1] : uc[PX - 1];
     const bool c1 = r > 0 && r + 1 < n1;
-    float nv[2][4], irv[4];
+    float nv0[PX], nv1[PX], irv[PX];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
+    for (int t = 0; t < PX; ++t) {
       const int x = x0 + t;
-      const double ul = t == 0 ? left : uc[t - 1], ur = t == 3 ? right : uc[t + 1];
+      const double ul = t == 0 ? left : uc[t - 1], ur = t == PX - 1 ? right : uc[t + 1];
       const bool hm = x > 0, hp = x < n0 - 1;
       const double dxl = hm ? ul : uc[t], dxr = hp ? ur : uc[t];
       const double dyl = r > 0 ? um[t] : uc[t], dyr = r + 1 < n1 ? up[t] : uc[t];
@@ -608,8 +669,8 @@ __global__ void __launch_bounds__(256, 2) k_ngf_sfeat2(const Args a, int seg, in
       const float g1 = (float)((dyr - dyl) * (c1 ? h1 : f1));
       const float rho = sqrtf(g0 * g0 + g1 * g1 + e2);
       const float ir = 1.f / rho;
-      nv[0][t] = g0 * ir;
-      nv[1][t] = g1 * ir;
+      nv0[t] = g0 * ir;
+      nv1[t] = g1 * ir;
       irv[t] = ir;
     }
     if (colok) {
@@ -618,26 +679,27 @@ __global__ void __launch_bounds__(256, 2) k_ngf_sfeat2(const Args a, int seg, in
       float* n1p = n0p + zstride;
       float* irp = IRho + (long long)k * zstride + (q - zlo);
       if (vz) {
-        *reinterpret_cast<float4*>(n0p) = make_float4(nv[0][0], nv[0][1], nv[0][2], nv[0][3]);
-        *reinterpret_cast<float4*>(n1p) = make_float4(nv[1][0], nv[1][1], nv[1][2], nv[1][3]);
-        *reinterpret_cast<float4*>(irp) = make_float4(irv[0], irv[1], irv[2], irv[3]);
+        VecF<PX>::st(n0p, nv0);
+        VecF<PX>::st(n1p, nv1);
+        VecF<PX>::st(irp, irv);
       } else {
 #pragma unroll
-        for (int t = 0; t < 4; ++t)
+        for (int t = 0; t < PX; ++t)
           if (x0 + t < n0) {
-            n0p[t] = nv[0][t];
-            n1p[t] = nv[1][t];
+            n0p[t] = nv0[t];
+            n1p[t] = nv1[t];
             irp[t] = irv[t];
           }
       }
     }
-    double un[4];
+    double un[PX];
     if (more) finish_row(r + 2, cr, un);
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
+    for (int t = 0; t < PX; ++t) {
       um[t] = uc[t];
       uc[t] = up[t];
       up[t] = more ? un[t] : up[t];
+      cr[t] = cn[t];
     }
   }
 }

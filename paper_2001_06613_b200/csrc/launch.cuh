@@ -301,20 +301,21 @@ struct NgfBufs {
 // not fit one CTA (n0 > 1024) or the ranges are not whole rows
 inline cudaError_t ngf_sfeat_d2(const Launch& L, const Args& a, const NgfBufs& B) {
   const int n0 = a.g.n[0];
-  if (a.g.nd != 2 || n0 > 1024 || (B.zlo % n0) || (B.zhi % n0) || (a.pix_lo % n0) || (a.pix_hi % n0))
+  if (a.g.nd != 2 || n0 > 1024 || (B.zlo % n0) || (B.zhi % n0) || (a.pix_lo % n0) || (a.pix_hi % n0))  // 512 x 2
     return cudaErrorNotSupported;
   const int rz0 = (int)(B.zlo / n0), rz1 = (int)(B.zhi / n0);
   const int rs0 = (int)(a.pix_lo / n0), rs1 = (int)(a.pix_hi / n0);
   int seg = 32;
   while (seg > 8 && (long long)((rz1 - rz0 + seg - 1) / seg) * a.K < 8LL * L.sms) seg /= 2;
   const dim3 grid((unsigned)((rz1 - rz0 + seg - 1) / seg), (unsigned)a.K);
-  const int nt = ((n0 + 3) / 4 + 31) / 32 * 32;
+  constexpr int PX = 2;  // columns per thread: 512 threads for a 1024-pixel row
+  const int nt = ((n0 + PX - 1) / PX + 31) / 32 * 32;
   if (a.g.pow2)
-    k_ngf_sfeat2<true><<<grid, nt, 0, L.stream>>>(a, seg, rz0, rz1, rs0, rs1, B.Nf, B.Rho, B.zlo, B.zstride, B.G,
-                                                  B.vlo, B.vstride);
+    k_ngf_sfeat2<true, PX><<<grid, nt, 0, L.stream>>>(a, seg, rz0, rz1, rs0, rs1, B.Nf, B.Rho, B.zlo, B.zstride,
+                                                      B.G, B.vlo, B.vstride);
   else
-    k_ngf_sfeat2<false><<<grid, nt, 0, L.stream>>>(a, seg, rz0, rz1, rs0, rs1, B.Nf, B.Rho, B.zlo, B.zstride, B.G,
-                                                   B.vlo, B.vstride);
+    k_ngf_sfeat2<false, PX><<<grid, nt, 0, L.stream>>>(a, seg, rz0, rz1, rs0, rs1, B.Nf, B.Rho, B.zlo, B.zstride,
+                                                       B.G, B.vlo, B.vstride);
   return cudaGetLastError();
 }
 
