@@ -297,26 +297,52 @@ struct TGX {
   static constexpr int ACC_ROWS = 128, ACC_COLS = KP == 128 ? 128 : N;
 };
 
+// Runtime shared-memory layout of k_gram_tcx: at KP = 128 the stage (= TMA box) and operand rows follow
+// KPN = K rounded up to 16 instead of 128, and the bytes saved buy TMA stages (K = 100: 4 instead of 2 —
+// a 16 KB tile takes longer to arrive than its four K8 steps take on the tensor core).
+struct GxLayout {
+  int rows;      // stage rows (frames per TMA box)
+  int nst;       // TMA stages
+  int sbytes;    // bytes per stage
+  int obytes;    // bytes per operand buffer
+  int acc_rows;  // fp64 accumulator rows (row width ACC_COLS)
+};
+constexpr int kGxMaxStages = 6;
+
 template <int KP>
-constexpr size_t tgx_smem() {
+inline GxLayout tgx_layout(int K, size_t smem_cap) {
   using C = TGX<KP>;
-  return 1024 + (size_t)C::NST * C::SBYTES + (size_t)C::NB * C::NOPS * C::OBYTES +
-         (size_t)C::ACC_ROWS * C::ACC_COLS * 8 + 512;
+  GxLayout L{};
+  const int kpn = (K + 15) / 16 * 16;
+  L.rows = KP == 128 ? kpn : KP;
+  L.sbytes = L.rows * C::TP * 4;
+  L.obytes = KP == 128 ? 2 * kpn * 128 : C::OBYTES;
+  L.acc_rows = KP == 128 ? kpn : C::ACC_ROWS;
+  const size_t fixed = 1024 + (size_t)C::NB * L.obytes + (size_t)L.acc_rows * C::ACC_COLS * 8 + 512;
+  int nst = smem_cap > fixed ? (int)((smem_cap - fixed) / L.sbytes) : 0;
+  L.nst = nst < 2 ? 2 : nst > kGxMaxStages ? kGxMaxStages : nst;
+  return L;
+}
+template <int KP>
+inline size_t tgx_smem(const GxLayout& L) {
+  using C = TGX<KP>;
+  return 1024 + (size_t)L.nst * L.sbytes + (size_t)C::NB * L.obytes + (size_t)L.acc_rows * C::ACC_COLS * 8 + 512;
 }
 
 template <int KP>
 __global__ void __launch_bounds__(TGX<KP>::NT, 1) k_gram_tcx(const Args a, const __grid_constant__ CUtensorMap xmap,
-                                                            int ntx, int ncomp) {
+                                                            int ntx, int ncomp, const GxLayout lay) {
   using C = TGX<KP>;
-  constexpr int TP = C::TP, NST = C::NST, NB = C::NB, NA = C::NA, NC = C::ACC_COLS;
+  constexpr int TP = C::TP, NB = C::NB, NA = C::NA, NC = C::ACC_COLS;
+  const int NST = lay.nst;
   extern __shared__ __align__(1024) unsigned char smem_gx[];
   unsigned char* base = smem_gx + ((1024 - (smem_u32(smem_gx) & 1023)) & 1023);
-  float* stage = reinterpret_cast<float*>(base);                                       // [NST][KP][32]
-  unsigned char* Vb = base + (size_t)NST * C::SBYTES;                                  // [NB][NOPS][128 x 32]
-  double* accs = reinterpret_cast<double*>(Vb + (size_t)NB * C::NOPS * C::OBYTES);     // [128][NC] swizzled
-  uint64_t* bars = reinterpret_cast<uint64_t*>(accs + C::ACC_ROWS * NC);
+  float* stage = reinterpret_cast<float*>(base);                                       // [NST][rows][TP]
+  unsigned char* Vb = base + (size_t)NST * lay.sbytes;                                 // [NB][operand]
+  double* accs = reinterpret_cast<double*>(Vb + (size_t)NB * lay.obytes);              // [acc_rows][NC] swizzled
+  uint64_t* bars = reinterpret_cast<uint64_t*>(accs + (size_t)lay.acc_rows * NC);
   uint64_t* st_full = bars;
-  uint64_t* vb_full = st_full + NST;
+  uint64_t* vb_full = st_full + kGxMaxStages;
   uint64_t* vb_free = vb_full + NB;
   uint64_t* acc_full = vb_free + NB;
   uint64_t* acc_free = acc_full + NA;
@@ -328,8 +354,8 @@ __global__ void __launch_bounds__(TGX<KP>::NT, 1) k_gram_tcx(const Args a, const
   const long long nloc = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   auto load_tile = [&](long long n, int st) {
     const long long t = blockIdx.x + n * gridDim.x;
-    mbar_arrive_expect_tx(&st_full[st], (uint32_t)C::SBYTES);
-    tma_load_3d(stage + (size_t)st * KP * TP, &xmap, (int)(t % ntx) * TP, (int)(t / ntx), 0, &st_full[st]);
+    mbar_arrive_expect_tx(&st_full[st], (uint32_t)lay.sbytes);
+    tma_load_3d(stage + (size_t)st * lay.rows * TP, &xmap, (int)(t % ntx) * TP, (int)(t / ntx), 0, &st_full[st]);
   };
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) mbar_init(&st_full[s], 1);
@@ -344,7 +370,7 @@ __global__ void __launch_bounds__(TGX<KP>::NT, 1) k_gram_tcx(const Args a, const
     fence_mbar_init();
     tma_prefetch_desc(&xmap);
   }
-  for (int e = tid; e < C::ACC_ROWS * NC; e += C::NT) accs[e] = 0.0;
+  for (int e = tid; e < lay.acc_rows * NC; e += C::NT) accs[e] = 0.0;
   const int KPN = KP == 128 ? (K + 15) / 16 * 16 : KP;  // rows of H (and of L) in the KP = 128 buffer
   constexpr int TS = C::N;                              // TMEM columns per slot
   if (warp == C::NSP / 32) tmem_alloc(tmem_slot, TS * NA);
@@ -364,12 +390,14 @@ __global__ void __launch_bounds__(TGX<KP>::NT, 1) k_gram_tcx(const Args a, const
     for (long long n = 0; n < nloc; ++n) {
       const int b = (int)(n % NB), st = (int)(n % NST);
       mbar_wait(&st_full[st], (uint32_t)((n / NST) & 1));
-      const float* src = stage + (size_t)st * KP * TP + (size_t)r * TP + part * CPT;
+      const bool rok = r < lay.rows;  // KP = 128: rows past KPN are not staged
+      const float* src = stage + (size_t)st * lay.rows * TP + (size_t)r * TP + part * CPT;
       float4 qq[CPT / 4];
 #pragma unroll
-      for (int h = 0; h < CPT / 4; ++h) qq[h] = *reinterpret_cast<const float4*>(src + 4 * h);
+      for (int h = 0; h < CPT / 4; ++h)
+        qq[h] = rok ? *reinterpret_cast<const float4*>(src + 4 * h) : make_float4(0.f, 0.f, 0.f, 0.f);
       if (n >= NB) mbar_wait(&vb_free[b], (uint32_t)((n / NB - 1) & 1));
-      unsigned char* ob = Vb + (size_t)b * C::NOPS * C::OBYTES;
+      unsigned char* ob = Vb + (size_t)b * lay.obytes;
 #pragma unroll
       for (int h = 0; h < CPT / 4; ++h) {
         const float qv[4] = {qq[h].x, qq[h].y, qq[h].z, qq[h].w};
@@ -413,7 +441,7 @@ __global__ void __launch_bounds__(TGX<KP>::NT, 1) k_gram_tcx(const Args a, const
         if (n + NST < nloc) load_tile(n + NST, st);
         if (first && grp >= NA) mbar_wait(&acc_free[s], (uint32_t)((grp / NA - 1) & 1));
         tc_fence_after();
-        const uint32_t o0 = smem_u32(Vb + (size_t)b * C::NOPS * C::OBYTES);
+        const uint32_t o0 = smem_u32(Vb + (size_t)b * lay.obytes);
         const uint32_t acc = tmem + (uint32_t)(s * TS);
         const uint32_t idesc = KP == 128 ? umma_idesc_tf32(128, 2 * KPN) : C::IDESC;
 #pragma unroll
@@ -433,7 +461,8 @@ __global__ void __launch_bounds__(TGX<KP>::NT, 1) k_gram_tcx(const Args a, const
   } else {
     // ======================= flushers: TMEM lane quarter q = warp % 4, row m = 32 q + lane
     const int q = warp & 3, m = 32 * q + lane;
-    double* arow = accs + (size_t)m * NC;
+    const bool mok = m < lay.acc_rows;  // KP = 128: TMEM lanes past KPN carry garbage rows (not accumulated)
+    double* arow = accs + (size_t)(mok ? m : 0) * NC;
     const long long ngrp = (nloc + C::R - 1) / C::R;
     for (long long n = 0; n < ngrp; ++n) {
       const int s = (int)(n % NA);
@@ -448,13 +477,15 @@ __global__ void __launch_bounds__(TGX<KP>::NT, 1) k_gram_tcx(const Args a, const
             tmem_ld32(ts + (uint32_t)c0, hh);
             tmem_ld32(ts + (uint32_t)(KPN + c0), hl);
 #pragma unroll
-            for (int cc = 0; cc < 32; ++cc) arow[(c0 + cc) ^ lane] += 0.5 * (double)hh[cc] + (double)hl[cc];
+            for (int cc = 0; cc < 32; ++cc)
+              if (mok) arow[(c0 + cc) ^ lane] += 0.5 * (double)hh[cc] + (double)hl[cc];
           } else {
             float hh[16], hl[16];
             tmem_ld16(ts + (uint32_t)c0, hh);
             tmem_ld16(ts + (uint32_t)(KPN + c0), hl);
 #pragma unroll
-            for (int cc = 0; cc < 16; ++cc) arow[(c0 + cc) ^ lane] += 0.5 * (double)hh[cc] + (double)hl[cc];
+            for (int cc = 0; cc < 16; ++cc)
+              if (mok) arow[(c0 + cc) ^ lane] += 0.5 * (double)hh[cc] + (double)hl[cc];
           }
         }
       } else {

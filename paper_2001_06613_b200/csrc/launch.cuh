@@ -333,7 +333,10 @@ cudaError_t run_ngf_pass1_kp(const Launch& L, const Args& a, const NgfBufs& B, d
   memset(&xmap, 0, sizeof xmap);
   cuuint64_t gdim[3] = {(cuuint64_t)npix, (cuuint64_t)D, (cuuint64_t)a.K};
   cuuint64_t gstr[2] = {(cuuint64_t)B.zstride * 4, (cuuint64_t)D * B.zstride * 4};
-  cuuint32_t box[3] = {(cuuint32_t)C::TP, 1, (cuuint32_t)KP};
+  int smem_cap = 0;
+  cudaDeviceGetAttribute(&smem_cap, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0);
+  const GxLayout lay = tgx_layout<KP>(a.K, (size_t)smem_cap);
+  cuuint32_t box[3] = {(cuuint32_t)C::TP, 1, (cuuint32_t)lay.rows};
   cuuint32_t es[3] = {1, 1, 1};
   if (fn(&xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, B.Nf + (a.pix_lo - B.zlo), gdim, gstr, box, es,
          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -354,7 +357,7 @@ cudaError_t run_ngf_pass1_kp(const Launch& L, const Args& a, const NgfBufs& B, d
     e = cudaGetLastError();
   }
   if (e != cudaSuccess) return e;
-  const size_t smem = tgx_smem<KP>();
+  const size_t smem = tgx_smem<KP>(lay);
   e = cudaFuncSetAttribute(k_gram_tcx<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int ntx = (int)((npix + C::TP - 1) / C::TP);
@@ -365,7 +368,7 @@ cudaError_t run_ngf_pass1_kp(const Launch& L, const Args& a, const NgfBufs& B, d
   if ((size_t)grid * stride > part_cap) grid = (int)(part_cap / stride);
   Args b = a;
   b.part = part;
-  k_gram_tcx<KP><<<grid, C::NT, smem, L.stream>>>(b, xmap, ntx, D);
+  k_gram_tcx<KP><<<grid, C::NT, smem, L.stream>>>(b, xmap, ntx, D, lay);
   *nblk = grid;
   return cudaGetLastError();
 }
