@@ -146,16 +146,6 @@ SR_API int sr_set_grid_ctas(sr_ctx* ctx, int32_t ctas);
  * Default: off. */
 SR_API int sr_set_sample_reuse(sr_ctx* ctx, int32_t enable);
 
-/* Prepare an fp32 frame stack for the texture-gather sampling path: the frames are copied
- * once into gather-capable CUDA arrays (block-linear; 3-D frames as stacked z-slices) cached
- * in the context under frames_dev.  Later calls whose frames_dev matches fetch each bilinear
- * 2x2 footprint with one texture gather (tld4) instead of four loads; results are identical.
- * Call again after modifying the frames in place; sr_frames_release drops the copy.  fp64
- * stacks and frames beyond the gather limits (32768 per 2-D extent) are left on global loads. */
-SR_API int sr_frames_prepare(sr_ctx* ctx, int32_t dtype, const void* frames_dev, int32_t nframes,
-                             const sr_grid* grid);
-SR_API int sr_frames_release(sr_ctx* ctx, const void* frames_dev);
-
 /* Per-frame intensity shift (the frame mean, in fp64 then cast to dtype) used to
  * centre the raw Gram sums before they are formed. */
 SR_API int sr_frame_shifts(sr_ctx* ctx, int32_t dtype, const void* frames_dev, int32_t nframes,

@@ -132,8 +132,6 @@ EXPORTS = {
     "sr_set_grid_ctas": (_c.c_int, [_P, _c.c_int32]),
     "sr_set_sample_reuse": (_c.c_int, [_P, _c.c_int32]),
     "sr_frame_shifts": (_c.c_int, [_P, _c.c_int32, _P, _c.c_int32, _c.c_int64, _P]),
-    "sr_frames_prepare": (_c.c_int, [_P, _c.c_int32, _P, _c.c_int32, _c.POINTER(SrGrid)]),
-    "sr_frames_release": (_c.c_int, [_P, _P]),
     "sr_corr_partial": (_c.c_int, [_P, _PROB, _P]),
     "sr_corr_finalize": (_c.c_int, [_P, _PROB, _P, _D, _c.c_double, _c.c_int64, _P]),
     "sr_grad": (_c.c_int, [_P, _PROB, _P, _P, _c.c_int64, _c.c_int64]),

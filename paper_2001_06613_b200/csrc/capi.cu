@@ -15,15 +15,6 @@
 
 using namespace sr;
 
-// fp32 frame stacks copied into gather-capable CUDA arrays (sr_frames_prepare)
-struct TexSet {
-  const void* ptr = nullptr;
-  int nframes = 0;
-  long long N = 0;
-  std::vector<cudaArray_t> arr;
-  std::vector<cudaTextureObject_t> tex;
-};
-
 namespace sr {
 namespace lbfgs {
 struct Workspace;
@@ -40,15 +31,8 @@ struct sr_ctx {
   int sms = 148;
   int grid_override = 0;
   int legacy = 0;  // SEQREG_B200_LEGACY=1: non-specialized kernels only
-  int dbg = 0;     // SEQREG_B200_DEBUG: profiling experiment bits
-  int ws2 = 0;     // SEQREG_B200_WS2=1: warp-specialized pass 2
-  int tex_enabled = 0;  // SEQREG_B200_TEX=1: texture-gather sampling (measured slower on B200)
   int tc = 1;      // SEQREG_B200_TC=0: SIMT Gram instead of tcgen05 in pass 1
-  int tc2 = 0;     // SEQREG_B200_TC2=1: tcgen05 pass 2
   int graphs = 1;  // SEQREG_B200_GRAPH=0: sr_evaluate launches its kernels one by one (no graph replay)
-  int mma = 1;     // SEQREG_B200_MMA: 1 = k_sample_v + k_gram_mma + k_pass2_mma, 2 = fused k_sample_gram,
-                   // 0 = k_sample_v + k_gram_tc (tcgen05) + k_pass2_stream
-  int split = 1;   // SEQREG_B200_SPLIT=0: fused tensor-core pass 1 instead of sampling kernel + Gram kernel
   float* vbuf = nullptr;  // split pass 1: V = v - shift, [K][vstride]
   size_t vbuf_bytes = 0;
   float* gbuf = nullptr;  // split pass 1 with the streaming pass 2: grad T, [K][d][vstride]
@@ -104,22 +88,8 @@ struct sr_ctx {
   size_t curv_part_cap = 0;
   int* iaux = nullptr;
   size_t iaux_cap = 0;
-  std::vector<TexSet> texsets;
-  int job_use_tex = 0;  // the uploaded job carries texture handles
 };
 
-static void texset_free(TexSet& t) {
-  for (auto o : t.tex) cudaDestroyTextureObject(o);
-  for (auto a : t.arr) cudaFreeArray(a);
-  t.tex.clear();
-  t.arr.clear();
-}
-
-static const TexSet* texset_find(sr_ctx* c, const void* ptr, int nframes, long long N) {
-  for (auto& t : c->texsets)
-    if (t.ptr == ptr && t.nframes == nframes && t.N == N) return &t;
-  return nullptr;
-}
 
 static thread_local std::string g_err;
 
@@ -254,8 +224,6 @@ static Args make_args(sr_ctx* ctx, const sr_problem* p) {
   a.pix_lo = p->pix_lo;
   a.pix_hi = p->pix_hi;
   a.eps = p->ngf_eps;
-  a.dbg = ctx->dbg;
-  a.use_tex = ctx->job_use_tex;
   return a;
 }
 
@@ -273,13 +241,6 @@ static void build_job(sr_ctx* ctx, const sr_problem* p, const double* weights, J
     for (int j = 0; j < p->k; ++j)
       for (int e = 0; e < na; ++e) nj.affine[j * 12 + e] = p->affine[j * na + e];
   }
-  {
-    long long N = 1;
-    for (int a2 = 0; a2 < p->grid.ndim; ++a2) N *= p->grid.dims[a2];
-    const TexSet* ts = (p->dtype == SR_F32 && ctx->tex_enabled) ? texset_find(ctx, p->frames_dev, p->nframes, N) : nullptr;
-    ctx->job_use_tex = ts != nullptr;
-    for (int j = 0; j < p->k; ++j) nj.tex[j] = ts ? (unsigned long long)ts->tex[p->frame_index[j]] : 0ull;
-  }
 }
 
 static int upload_job(sr_ctx* ctx, const sr_problem* p, const double* weights) {
@@ -296,7 +257,7 @@ static int upload_job(sr_ctx* ctx, const sr_problem* p, const double* weights) {
 }
 
 static Launch launch_of(sr_ctx* ctx) {
-  return Launch{ctx->stream, ctx->sms, ctx->grid_override, ctx->legacy, ctx->ws2, ctx->tc, ctx->split, ctx->tc2};
+  return Launch{ctx->stream, ctx->sms, ctx->grid_override, ctx->legacy, ctx->tc};
 }
 
 #define SR_SWITCH(dtype, nd, FN, ...)                                    \
@@ -311,18 +272,12 @@ static cudaError_t launch_reduce_finalize(sr_ctx* c, const sr_problem* p, int nb
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(dsm, 1));
   if (e != cudaSuccess) return e;
   const int stride = KP * KP + 3 * KP;
-  // PDL (SEQREG_B200_PDL=1, off by default: measured slower): may start while pass 1 drains
-  static const bool pdl = getenv("SEQREG_B200_PDL") && getenv("SEQREG_B200_PDL")[0] == '1';
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((stride + 31) / 32);
   cfg.blockDim = dim3(1024);
   cfg.dynamicSmemBytes = dsm;
   cfg.stream = c->stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = 0;
   return cudaLaunchKernelEx(&cfg, kern, (const double*)c->part, nblk, KP, (int)p->k, count, raw, do_final,
                             (const Job*)c->job_dev, (int)p->feature, (int)p->grid.ndim, h, (const T*)p->shifts_dev,
                             stats, c->ticket);
@@ -334,14 +289,14 @@ static cudaError_t launch_reduce_finalize(sr_ctx* c, const sr_problem* p, int nb
 // the split NGF path: fp32 displacement fields, K <= 128, tensor-core Gram (KP = 128 partials)
 static bool ngf_split(const sr_ctx* c, const sr_problem* p) {
   return p->dtype == SR_F32 && p->feature == SR_NGF && p->param == SR_DISPLACEMENT && p->k <= 128 && !c->legacy &&
-         c->tc && c->split;
+         c->tc;
 }
 
 static int pass1_kp(const sr_ctx* c, const sr_problem* p) {
   if (p->dtype == SR_F32 && p->feature == SR_NCC && p->param == SR_DISPLACEMENT && p->k <= 32 && !c->legacy &&
       c->tc)
     return 32;
-  if (ngf_split(c, p)) return p->k <= 32 && c->mma ? 32 : p->k <= 64 ? 64 : 128;  // 32: TMA-fed mma.sync Gram
+  if (ngf_split(c, p)) return p->k <= 32 ? 32 : p->k <= 64 ? 64 : 128;  // 32: TMA-fed mma.sync Gram
   return kp_of(p->k);
 }
 
@@ -423,31 +378,24 @@ static int corr_partial_impl(sr_ctx* c, const sr_problem* p, double* raw, double
     } else {  // layout the tensor map cannot express: the generic kernels with the same KP layout
       CK(SR_SWITCH(p->dtype, p->grid.ndim, pass1, p->feature, p->param, KP, L, a, c->part, c->part_cap, &nblk));
     }
-  } else if (KP == 32 && p->dtype == SR_F32 && p->feature == SR_NCC && p->param == SR_DISPLACEMENT && c->split &&
-             c->tc && !c->legacy && npix > 0) {
+  } else if (KP == 32 && p->dtype == SR_F32 && p->feature == SR_NCC && p->param == SR_DISPLACEMENT && c->tc &&
+             !c->legacy && npix > 0) {
+    // split NCC pass 1: k_sample_vp (V = v - shift and grad T) + the TMA-fed mma.sync Gram (engine_mma.cuh);
+    // SEQREG_B200_P2S=0 leaves V, grad T unused by pass 2 (which then re-gathers)
     const long long vstride = (npix + 3) & ~3LL;  // V = v - shift, [K][vstride]
     void* vb = c->vbuf;
     rc = ensure(&vb, &c->vbuf_bytes, (size_t)p->k * vstride * 4);
     if (rc) return rc;
     c->vbuf = (float*)vb;
-    float* G = nullptr;
-    if (c->p2s) {
-      void* gb = c->gbuf;
-      rc = ensure(&gb, &c->gbuf_bytes, (size_t)p->k * p->grid.ndim * vstride * 4);
-      if (rc) return rc;
-      c->gbuf = (float*)gb;
-      G = c->gbuf;
-    }
+    void* gb = c->gbuf;
+    rc = ensure(&gb, &c->gbuf_bytes, (size_t)p->k * p->grid.ndim * vstride * 4);
+    if (rc) return rc;
+    c->gbuf = (float*)gb;
+    float* G = c->gbuf;
     c->vtag.valid = 0;
-    if (G && c->mma == 2)  // fused sampling + mma.sync Gram (engine_mma.cuh; measured slower)
-      CK(p->grid.ndim == 2 ? sample_gram_d2(L, a, c->vbuf, G, vstride, c->part, c->part_cap, &nblk)
-                           : sample_gram_d3(L, a, c->vbuf, G, vstride, c->part, c->part_cap, &nblk));
-    else if (G && c->mma)  // k_sample_v + mma.sync Gram kernel (engine_mma.cuh)
-      CK(p->grid.ndim == 2 ? sample_then_gram_d2(L, a, c->vbuf, G, vstride, c->part, c->part_cap, &nblk)
-                           : sample_then_gram_d3(L, a, c->vbuf, G, vstride, c->part, c->part_cap, &nblk));
-    else if (p->grid.ndim == 2) CK(pass1_split_d2(L, a, c->vbuf, G, vstride, c->part, c->part_cap, &nblk));
-    else CK(pass1_split_d3(L, a, c->vbuf, G, vstride, c->part, c->part_cap, &nblk));
-    set_vtag(c, p, vstride, G != nullptr);
+    CK(p->grid.ndim == 2 ? sample_then_gram_d2(L, a, c->vbuf, G, vstride, c->part, c->part_cap, &nblk)
+                         : sample_then_gram_d3(L, a, c->vbuf, G, vstride, c->part, c->part_cap, &nblk));
+    set_vtag(c, p, vstride, c->p2s);
   } else {
     c->vtag.valid = 0;
     CK(SR_SWITCH(p->dtype, p->grid.ndim, pass1, p->feature, p->param, KP, L, a, c->part, c->part_cap, &nblk));
@@ -527,26 +475,16 @@ int sr_create(int32_t device, sr_ctx** out) {
   CK(cudaGetDeviceProperties(&prop, device));
   c->sms = prop.multiProcessorCount;
   {
+    // A/B switches kept for the test suite (tests/test_variants_gpu.py): every one keeps results within
+    // tolerance; the slower kernel variants of round 1 were removed
     const char* lg = getenv("SEQREG_B200_LEGACY");
     c->legacy = (lg && lg[0] == '1') ? 1 : 0;
-    const char* db = getenv("SEQREG_B200_DEBUG");
-    c->dbg = db ? atoi(db) : 0;
-    const char* w2 = getenv("SEQREG_B200_WS2");
-    c->ws2 = (w2 && w2[0] == '1') ? 1 : 0;
-    const char* tx = getenv("SEQREG_B200_TEX");
-    c->tex_enabled = (tx && tx[0] == '1') ? 1 : 0;
     const char* tcs = getenv("SEQREG_B200_TC");
     c->tc = (tcs && tcs[0] == '0') ? 0 : 1;
-    const char* sp = getenv("SEQREG_B200_SPLIT");
-    c->split = (sp && sp[0] == '0') ? 0 : 1;
     const char* ps = getenv("SEQREG_B200_P2S");
     c->p2s = (ps && ps[0] == '0') ? 0 : 1;
-    const char* t2 = getenv("SEQREG_B200_TC2");
-    c->tc2 = (t2 && t2[0] == '1') ? 1 : 0;
     const char* gr = getenv("SEQREG_B200_GRAPH");
     c->graphs = (gr && gr[0] == '0') ? 0 : 1;
-    const char* mm = getenv("SEQREG_B200_MMA");
-    c->mma = mm ? atoi(mm) : 1;
   }
   CK(cudaMalloc(&c->job_dev, sizeof(Job)));
   CK(cudaMalloc(&c->ticket, sizeof(unsigned)));
@@ -571,7 +509,6 @@ int sr_destroy(sr_ctx* c) {
   cudaFree(c->vbuf);
   cudaFree(c->gbuf);
   cudaFree(c->ngfbuf);
-  for (auto& t : c->texsets) texset_free(t);
   cudaFree(c->zbuf);
   cudaFree(c->aux);
   cudaFree(c->iaux);
@@ -617,79 +554,6 @@ int sr_set_grid_ctas(sr_ctx* c, int32_t ctas) {
   return SR_OK;
 }
 
-int sr_frames_prepare(sr_ctx* c, int32_t dtype, const void* frames, int32_t nframes, const sr_grid* grid) {
-  if (!c || !frames || !grid || nframes < 1) return fail(SR_ERR_ARG, "bad sr_frames_prepare arguments");
-  int rc = check_grid(*grid);
-  if (rc) return rc;
-  if (dtype != SR_F32 || !c->tex_enabled) return SR_OK;  // fp64 frames (and the default) use global loads
-  const int n0 = grid->dims[0];
-  long long rows = 1;
-  for (int a = 1; a < grid->ndim; ++a) rows *= grid->dims[a];
-  if (n0 > 32768 || rows > 32768) return SR_OK;  // beyond the texture-gather limits: global loads
-  CK(cudaSetDevice(c->device));
-  for (auto it = c->texsets.begin(); it != c->texsets.end(); ++it)
-    if (it->ptr == frames) {
-      CK(cudaStreamSynchronize(c->stream));
-      texset_free(*it);
-      c->texsets.erase(it);
-      break;
-    }
-  TexSet t;
-  t.ptr = frames;
-  t.nframes = nframes;
-  t.N = (long long)n0 * rows;
-  const cudaChannelFormatDesc desc = cudaCreateChannelDesc<float>();
-  for (int f = 0; f < nframes; ++f) {
-    cudaArray_t arr = nullptr;
-    cudaError_t e = cudaMallocArray(&arr, &desc, n0, (size_t)rows, cudaArrayTextureGather);
-    if (e != cudaSuccess) {
-      texset_free(t);
-      return fail(SR_ERR_CUDA, "cudaMallocArray failed: %s", cudaGetErrorString(e));
-    }
-    t.arr.push_back(arr);
-    const float* src = reinterpret_cast<const float*>(frames) + (long long)f * t.N;
-    e = cudaMemcpy2DToArrayAsync(arr, 0, 0, src, (size_t)n0 * 4, (size_t)n0 * 4, (size_t)rows,
-                                 cudaMemcpyDeviceToDevice, c->stream);
-    if (e != cudaSuccess) {
-      texset_free(t);
-      return fail(SR_ERR_CUDA, "cudaMemcpy2DToArrayAsync failed: %s", cudaGetErrorString(e));
-    }
-    cudaResourceDesc res;
-    std::memset(&res, 0, sizeof res);
-    res.resType = cudaResourceTypeArray;
-    res.res.array.array = arr;
-    cudaTextureDesc td;
-    std::memset(&td, 0, sizeof td);
-    td.addressMode[0] = cudaAddressModeClamp;
-    td.addressMode[1] = cudaAddressModeClamp;
-    td.filterMode = cudaFilterModePoint;
-    td.readMode = cudaReadModeElementType;
-    td.normalizedCoords = 0;
-    cudaTextureObject_t tex = 0;
-    e = cudaCreateTextureObject(&tex, &res, &td, nullptr);
-    if (e != cudaSuccess) {
-      texset_free(t);
-      return fail(SR_ERR_CUDA, "cudaCreateTextureObject failed: %s", cudaGetErrorString(e));
-    }
-    t.tex.push_back(tex);
-  }
-  c->texsets.push_back(std::move(t));
-  c->job_valid = false;  // handles may have changed
-  return SR_OK;
-}
-
-int sr_frames_release(sr_ctx* c, const void* frames) {
-  if (!c) return fail(SR_ERR_ARG, "null context");
-  for (auto it = c->texsets.begin(); it != c->texsets.end(); ++it)
-    if (it->ptr == frames) {
-      CK(cudaStreamSynchronize(c->stream));
-      texset_free(*it);
-      c->texsets.erase(it);
-      c->job_valid = false;
-      break;
-    }
-  return SR_OK;
-}
 
 int sr_frame_shifts(sr_ctx* c, int32_t dtype, const void* frames, int32_t nframes, int64_t n,
                     void* shifts) {
@@ -750,7 +614,7 @@ static int grad_impl_core(sr_ctx* c, const sr_problem* p, const double* stats, v
     a.o_stride = g_stride;
     if (reuse && p->dtype == SR_F32 && p->param == SR_DISPLACEMENT && p->k <= 32 && vtag_matches(c, p)) {
       const long long lim = 1LL << 31;  // k_pass2_mma uses 32-bit element offsets
-      if (c->mma && (long long)p->k * d * c->vtag.vstride < lim && (long long)p->k * d * g_stride < lim)
+      if ((long long)p->k * d * c->vtag.vstride < lim && (long long)p->k * d * g_stride < lim)
         CK(d == 2 ? pass2_mma_d2(L, a, c->vbuf, c->gbuf, c->vtag.vstride)
                   : pass2_mma_d3(L, a, c->vbuf, c->gbuf, c->vtag.vstride));
       else
@@ -906,7 +770,7 @@ int sr_evaluate(sr_ctx* c, const sr_problem* p, const double* weights, double ce
   CK(cudaSetDevice(c->device));
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   CK(cudaStreamIsCapturing(c->stream, &cs));
-  if (!c->graphs || c->tex_enabled || cs != cudaStreamCaptureStatusNone) {  // (the caller may be capturing)
+  if (!c->graphs || cs != cudaStreamCaptureStatusNone) {  // (the caller may be capturing)
     rc = upload_job(c, p, weights);
     if (rc) return rc;
     return evaluate_impl(c, p, cell_volume, raw_dev, stats_dev, grad_dev);

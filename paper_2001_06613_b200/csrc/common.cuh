@@ -46,7 +46,6 @@ struct Job {
   int frame_index[kMaxFrames];
   double weights[kMaxFrames];
   double affine[kMaxFrames * 12];
-  unsigned long long tex[kMaxFrames];  // fp32 frames as gather textures (0 = none), per subset position
 };
 
 // ---------------------------------------------------------------- rounding ops
@@ -279,69 +278,6 @@ __device__ __forceinline__ void interp2_prep(const Geo& g, P px, P py, int& base
   base = (int)l0 + (int)l1 * g.sti[1];
 }
 
-
-// ---- bilinear / trilinear sampling through the texture unit (fp32 frames prepared as
-// CUDA arrays, see sr_frames_prepare).  The 2x2 footprint is fetched with one tld4 at the
-// texel-space coordinate (i0 + 1, r0 + 1), i.e. exactly the corners the reference uses
-// (i0 = min(floor(tc), n - 2)); the texels come back unfiltered, so results are identical
-// to the global-load path.  gather order: x=(i0,r0+1) y=(i0+1,r0+1) z=(i0+1,r0) w=(i0,r0).
-template <int D, bool GRAD, bool POW2>
-__device__ __forceinline__ float interp_tex(unsigned long long tex, const Geo& g, const float (&p)[D],
-                                            float (&gr)[D]) {
-  bool inside = true;
-  float f[D], fl[D];
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-    const float q = __fsub_rn(p[a], g.of[a]);
-    const float t = POW2 ? fmaf(q, g.invf[a], -0.5f) : __fsub_rn(__fdiv_rn(q, g.sf[a]), 0.5f);
-    const float hi = (float)(g.n[a] - 1);
-    const float tc = fminf(fmaxf(t, 0.f), hi);
-    inside = inside && (tc == t);
-    fl[a] = fminf(floorf(tc), hi - 1.f);
-    f[a] = tc - fl[a];
-  }
-  const cudaTextureObject_t to = (cudaTextureObject_t)tex;
-  float val, gv[D];
-  if (D == 2) {
-    const float4 c = tex2Dgather<float4>(to, fl[0] + 1.f, fl[1] + 1.f, 0);
-    const float v00 = c.w, v10 = c.z, v01 = c.x, v11 = c.y;
-    const float d0 = v10 - v00, d1 = v11 - v01;
-    const float a0 = fmaf(f[0], d0, v00), a1 = fmaf(f[0], d1, v01);
-    const float e = a1 - a0;
-    val = fmaf(f[1], e, a0);
-    if (GRAD) {
-      gv[0] = fmaf(f[1], d1 - d0, d0);
-      gv[1] = e;
-    }
-  } else {
-    const float r0 = fl[1] + fl[D - 1] * (float)g.n[1];
-    const float4 c0 = tex2Dgather<float4>(to, fl[0] + 1.f, r0 + 1.f, 0);
-    const float4 c1 = tex2Dgather<float4>(to, fl[0] + 1.f, r0 + (float)g.n[1] + 1.f, 0);
-    // a[c1][c2]: lerp along axis 0 at (row offset c1, slice offset c2)
-    const float d00 = c0.z - c0.w, d10 = c0.y - c0.x, d01 = c1.z - c1.w, d11 = c1.y - c1.x;
-    const float a00 = fmaf(f[0], d00, c0.w), a10 = fmaf(f[0], d10, c0.x);
-    const float a01 = fmaf(f[0], d01, c1.w), a11 = fmaf(f[0], d11, c1.x);
-    const float e0 = a10 - a00, e1 = a11 - a01;
-    const float b0 = fmaf(f[1], e0, a00), b1 = fmaf(f[1], e1, a01);
-    const float eb = b1 - b0;
-    val = fmaf(f[D - 1], eb, b0);
-    if (GRAD) {
-      const float dz0 = fmaf(f[1], d10 - d00, d00);
-      const float dz1 = fmaf(f[1], d11 - d01, d01);
-      gv[0] = fmaf(f[D - 1], dz1 - dz0, dz0);
-      gv[1] = fmaf(f[D - 1], e1 - e0, e0);
-      gv[D - 1] = eb;
-    }
-  }
-  if (GRAD) {
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      const float gg = POW2 ? gv[a] * g.invf[a] : gv[a] / g.sf[a];
-      gr[a] = inside ? gg : 0.f;
-    }
-  }
-  return inside ? val : 0.f;
-}
 
 // Flat pixel index -> integer coordinates.
 template <int D>

@@ -41,9 +41,7 @@ struct Args {
   void* out;            // pass 2 output: grad (disp) / z buffer (NGF)
   long long o_off, o_stride;
   double* part_aff;     // pass 2 affine partials
-  int dbg;              // SEQREG_B200_DEBUG bits (profiling experiments only)
   int ymap_ok;          // a y tensor map was encoded for the warp-specialized kernels
-  int use_tex;          // job->tex[] holds gather textures of the subset frames (fp32)
   double curv_alpha;    // > 0: pass 2 adds the curvature gradient alpha h L L (y - x) (sr_evaluate_reg)
   double curv_h;
   double* curv_part;    // per-CTA partial sums of S (reduced by k_reduce)
@@ -155,9 +153,6 @@ __device__ __forceinline__ T sample_at(const Args& a, const T* img, int j, long 
                                        const int (&c)[3], T (&gr)[D]) {
   P p[D];
   warp_point<T, P, D, PARAM>(a, j, pix, c, p);
-  if constexpr (std::is_same<T, float>::value && std::is_same<P, float>::value) {
-    if (a.use_tex) return interp_tex<D, GRAD, POW2>(a.job->tex[j], a.g, p, gr);
-  }
   return interp<T, P, D, GRAD, POW2>(img, a.g, p, gr);
 }
 
@@ -189,34 +184,19 @@ __device__ __forceinline__ void sample_quad(const Args& a, const T* img, int j, 
       warp_point<T, P, D, PARAM>(a, j, p0 + e, c, p[e]);
     }
   }
-  if constexpr (std::is_same<T, float>::value && std::is_same<P, float>::value) {
-    if (a.use_tex) {
-      const unsigned long long tx = a.job->tex[j];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) v[e] = interp_tex<D, GRAD, POW2>(tx, a.g, p[e], gr[e]);
-      return;
-    }
-  }
 #pragma unroll
   for (int e = 0; e < 4; ++e) v[e] = interp<T, P, D, GRAD, POW2>(img, a.g, p[e], gr[e]);
 }
 
-// Interpolate four prepared points (the quad's y already in registers); tex != 0 uses the
-// texture-gather path (fp32 only).
+// Interpolate four prepared points (the quad's y already in registers).
 template <typename T, typename P, int D, bool GRAD, bool POW2>
 __device__ __forceinline__ void sample_pts4(const T* img, const Geo& g, const T (&yq)[D][4], T (&v)[4],
-                                            T (&gr)[4][D], unsigned long long tex = 0ull) {
+                                            T (&gr)[4][D]) {
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     P p[D];
 #pragma unroll
     for (int c = 0; c < D; ++c) p[c] = (P)yq[c][e];
-    if constexpr (std::is_same<T, float>::value && std::is_same<P, float>::value) {
-      if (tex) {
-        v[e] = interp_tex<D, GRAD, POW2>(tex, g, p, gr[e]);
-        continue;
-      }
-    }
     v[e] = interp<T, P, D, GRAD, POW2>(img, g, p, gr[e]);
   }
 }
@@ -373,8 +353,7 @@ __device__ __forceinline__ void pass1_body(const Args& a) {
           const T* img = frames + (long long)fi * a.g.N;
           const T sh = shifts ? shifts[fi] : (T)0;
           T v[4], gr[4][D];
-          if (PARAM == DISP) sample_pts4<T, P, D, false, POW2>(img, a.g, ypf[PARAM == DISP ? i : 0], v, gr,
-                                                               a.use_tex ? a.job->tex[k] : 0ull);
+          if (PARAM == DISP) sample_pts4<T, P, D, false, POW2>(img, a.g, ypf[PARAM == DISP ? i : 0], v, gr);
           else sample_quad<T, P, D, PARAM, false, POW2>(a, img, k, p0, nvalid, false, crd + 12 * q, v, gr);
           T out[4];
 #pragma unroll

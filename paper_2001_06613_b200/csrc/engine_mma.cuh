@@ -1,15 +1,13 @@
 // engine_mma.cuh — the fp32 NCC displacement-field path (K <= 32) with both K x K contractions on
-// the warp-level tensor path (mma.sync.m16n8k8 tf32, 3xTF32), fused into the memory-bound kernels:
+// the warp-level tensor path (mma.sync tf32, 3xTF32), plus the K <= 32 NGF z contraction (f16):
 //
-//   k_sample_gram  (pass 1): sample every subset frame of a 128-pixel tile (value + interpolant
-//                  gradient, grid.py:199-253), write V = v - shift and grad T for pass 2, keep the
-//                  tile's V as hi/lo tf32 rows in shared memory and form the tile's raw Gram
-//                  G = sum_p V V^T on the tensor cores (fp32 per tile, fp64 across tiles), plus the
-//                  per-frame sum / max / min.  Replaces k_sample_v + k_gram_tc (one HBM round trip
-//                  of V and the Gram kernel's pipeline latency disappear).
-//   k_pass2_mma    (pass 2): q = M'^T V + beta' for 16 pixels x 32 frames per warp on the tensor
+//   k_gram_tma / k_gram_mma (pass 1b): the raw Gram G = sum_p V V^T of the sampled values V = v - shift
+//                  (written by k_sample_vp, engine_tc.cuh) and the per-frame sum / max / min;
+//                  TMA-fed (default) or register-fed.
+//   k_pass2_tma / k_pass2_mma (pass 2): q = M'^T V + beta' for the pixels of a warp on the tensor
 //                  cores (M' fragments in shared memory), dD/dy_j = q_j grad T_j (similarity.py:
 //                  203-217 restated in DESIGN.md §3.3).  A pure stream: V, grad T in, dD/dy out.
+//   k_ngf_z_f16    (split NGF pass 2, K <= 32): r = M'^T n, z = (r - n (n.r)) / rho.
 //
 // 3xTF32: x = hi + lo with hi = tf32(x), lo = x - hi; a.b ~ hi_a hi_b + lo_a hi_b + hi_a lo_b (the
 // lo*lo term, 2^-22 relative, is dropped) — fp32-class products, fp32 accumulation inside a tile.
@@ -40,177 +38,13 @@ __device__ __forceinline__ void mma_tf32_k4(float (&c)[4], uint32_t a0, uint32_t
       : "r"(a0), "r"(a1), "r"(b0));
 }
 
-struct SG {
-  static constexpr int KP = 32, TP = 128, NT = 256;
-  static constexpr int LD = TP + 8;  // row stride (words) of the V tiles: 8-word skew per frame row
-};
-
-// Position of pixel p of a tile inside a V row: the fragment pair (t, t + 4) of every 8-pixel
-// k-step is stored adjacently so that one 64-bit shared load fetches it (conflict-free with LD = 136).
-__device__ __forceinline__ int sg_pos(int p) { return (p & ~7) | ((p & 3) << 1) | ((p >> 2) & 1); }
-
-// Pass 1.  Grid: persistent over 128-pixel tiles of the slab.  Sampling: warp w owns frames
-// 4w .. 4w+3 (nf = how many of them are < K), lanes consecutive pixels (p = lane + 32 e), four samples
-// in flight; the y of the next (tile, frame) unit is loaded before the current unit's gathers, so
-// only the gathers' latency is exposed.  Gram: warp w owns the m16 x n8 output block
-// (16 (w >> 2) .., 8 (w & 3) ..) of the 32 x 32 Gram.
-// Partials per CTA (the k_reduce_finalize layout): [G 32x32 | sum 32 | max 32 | -min 32] fp64.
-template <int D, bool POW2, int MINB>
-__global__ void __launch_bounds__(SG::NT, MINB) k_sample_gram(const Args a, float* __restrict__ V,
-                                                            float* __restrict__ G, long long vstride) {
-  constexpr int KP = SG::KP, TP = SG::TP, LD = SG::LD;
-  __shared__ __align__(16) float Vh[KP * LD];
-  __shared__ __align__(16) float Vl[KP * LD];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int K = a.K;
-  const long long npix = a.pix_hi - a.pix_lo;
-  const long long ntiles = (npix + TP - 1) / TP;
-  const uint64_t pol_first = l2_policy_evict_first(), pol_last = l2_policy_evict_last();
-  // rows K..31 stay zero (never written in the loop)
-  for (int e = tid; e < (KP - K) * LD; e += SG::NT) {
-    Vh[K * LD + e] = 0.f;
-    Vl[K * LD + e] = 0.f;
-  }
-  const float* shifts = reinterpret_cast<const float*>(a.shifts);
-  const float* yg = reinterpret_cast<const float*>(a.y) + (a.pix_lo - a.y_off);
-  const int k0 = 4 * warp, nf = max(0, min(4, K - k0));
-  float shv[4];
-#pragma unroll
-  for (int f = 0; f < 4; ++f) shv[f] = shifts ? shifts[a.job->frame_index[min(k0 + f, K - 1)]] : 0.f;
-  float fsum[4], fmx[4], fmn[4];
-#pragma unroll
-  for (int f = 0; f < 4; ++f) {
-    fsum[f] = 0.f;
-    fmx[f] = -INFINITY;
-    fmn[f] = INFINITY;
-  }
-  double gacc[4] = {0.0, 0.0, 0.0, 0.0};
-  const int g = lane >> 2, t = lane & 3;
-  const int mi = warp >> 2, ni = warp & 3;
-  // y of unit (tile, frame k0 + f): rows (k0 + f) D + c, pixels tile TP + lane + 32 e (clamped into the slab)
-  auto load_y = [&](long long tile, int f, float (&p)[4][D]) {
-    const long long p0 = tile * TP;
-    const int nb = (int)min(npix - p0, (long long)TP);
-    const float* yb = yg + (long long)((k0 + f) * D) * a.y_stride + p0;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int pe = min(lane + 32 * e, nb - 1);
-#pragma unroll
-      for (int c = 0; c < D; ++c) p[e][c] = ldg_hint_nv(yb + (long long)c * a.y_stride + pe, pol_first);
-    }
-  };
-  float pc[4][D];
-  if (nf > 0 && (long long)blockIdx.x < ntiles) load_y(blockIdx.x, 0, pc);
-  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const long long p0 = tile * TP;
-    const int nb = (int)min(npix - p0, (long long)TP);
-    const bool full = nb == TP;
-    // ---------------------------------------------------------------- sampling
-#pragma unroll
-    for (int f = 0; f < 4; ++f) {
-      if (f < nf) {  // warp-uniform
-        const int k = k0 + f;
-        // prefetch the next unit's y: the next frame of this tile, else frame k0 of the next tile
-        float pn[4][D];
-        const bool more = f + 1 < nf;
-        const long long nt = more ? tile : tile + gridDim.x;
-        if (more || nt < ntiles) load_y(nt, more ? f + 1 : 0, pn);
-        const float* img = reinterpret_cast<const float*>(a.frames) + (long long)a.job->frame_index[k] * a.g.N;
-        float v[4], gd[4][D];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) v[e] = interp<float, float, D, true, POW2>(img, a.g, pc[e], gd[e]);
-        float* vb = V + (long long)k * vstride + p0;
-        float* gb = G + (long long)(k * D) * vstride + p0;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int pe = lane + 32 * e;
-          const bool ok = full || pe < nb;
-          const float o = ok ? v[e] - shv[f] : 0.f;
-          if (ok) {
-            stg_hint(vb + pe, o, pol_last);
-#pragma unroll
-            for (int c = 0; c < D; ++c) stg_hint(gb + (long long)c * vstride + pe, gd[e][c], pol_last);
-            fmx[f] = fmaxf(fmx[f], o);
-            fmn[f] = fminf(fmn[f], o);
-          }
-          fsum[f] += o;
-          const float hi = to_tf32(o);
-          const int q = k * LD + sg_pos(pe);
-          Vh[q] = hi;
-          Vl[q] = o - hi;
-        }
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-#pragma unroll
-          for (int c = 0; c < D; ++c) pc[e][c] = pn[e][c];
-      }
-    }
-    __syncthreads();
-    // ---------------------------------------------------------------- Gram block on the tensor cores
-    float acc[2][3][4] = {};
-    const float* ah0 = Vh + (16 * mi + g) * LD + 2 * t;
-    const float* ah1 = ah0 + 8 * LD;
-    const float* al0 = Vl + (16 * mi + g) * LD + 2 * t;
-    const float* al1 = al0 + 8 * LD;
-    const float* bh = Vh + (8 * ni + g) * LD + 2 * t;
-    const float* bl = Vl + (8 * ni + g) * LD + 2 * t;
-#pragma unroll 8
-    for (int ks = 0; ks < TP / 8; ++ks) {
-      const int o = 8 * ks;
-      const float2 h0 = *reinterpret_cast<const float2*>(ah0 + o), h1 = *reinterpret_cast<const float2*>(ah1 + o);
-      const float2 l0 = *reinterpret_cast<const float2*>(al0 + o), l1 = *reinterpret_cast<const float2*>(al1 + o);
-      const float2 b_h = *reinterpret_cast<const float2*>(bh + o), b_l = *reinterpret_cast<const float2*>(bl + o);
-      const uint32_t AH[4] = {__float_as_uint(h0.x), __float_as_uint(h1.x), __float_as_uint(h0.y),
-                              __float_as_uint(h1.y)};
-      const uint32_t AL[4] = {__float_as_uint(l0.x), __float_as_uint(l1.x), __float_as_uint(l0.y),
-                              __float_as_uint(l1.y)};
-      float(&c3)[3][4] = acc[ks & 1];  // independent accumulator chains (HMMA latency)
-      mma_tf32(c3[0], AH, __float_as_uint(b_h.x), __float_as_uint(b_h.y));
-      mma_tf32(c3[1], AL, __float_as_uint(b_h.x), __float_as_uint(b_h.y));
-      mma_tf32(c3[2], AH, __float_as_uint(b_l.x), __float_as_uint(b_l.y));
-    }
-#pragma unroll
-    for (int r = 0; r < 4; ++r)
-      gacc[r] += (double)(((acc[0][0][r] + acc[1][0][r]) + (acc[0][1][r] + acc[1][1][r])) +
-                          (acc[0][2][r] + acc[1][2][r]));
-    __syncthreads();
-  }
-  // ---------------------------------------------------------------- per-CTA partials
-  double* out = a.part + (size_t)blockIdx.x * (KP * KP + 3 * KP);
-  {
-    const int i0 = 16 * mi + g, j0 = 8 * ni + 2 * t;
-    out[i0 * KP + j0] = gacc[0];
-    out[i0 * KP + j0 + 1] = gacc[1];
-    out[(i0 + 8) * KP + j0] = gacc[2];
-    out[(i0 + 8) * KP + j0 + 1] = gacc[3];
-  }
-#pragma unroll
-  for (int f = 0; f < 4; ++f) {
-    const int k = k0 + f;
-    double s = (double)fsum[f];
-    float mx = fmx[f], mn = fmn[f];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      s += __shfl_xor_sync(0xffffffffu, s, o);
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-    }
-    if (lane == 0) {
-      const double sh = k < K ? (double)shv[f] : 0.0;
-      out[KP * KP + k] = k < K ? s : 0.0;
-      out[KP * KP + KP + k] = (double)mx + sh;
-      out[KP * KP + 2 * KP + k] = -((double)mn + sh);
-    }
-  }
-}
-
 __device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t addr) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"(addr));
 }
 
-// Split pass 1, Gram kernel (after k_sample_v wrote V = v - shift as [K][vstride], mostly still in L2).
+// Split pass 1, Gram kernel (after k_sample_vp wrote V = v - shift as [K][vstride], mostly still in L2).
 // Persistent CTAs over 128-pixel tiles.  Load: warp w reads rows 4w .. 4w+3 of the tile, lane l
 // columns 4l .. 4l+3 (one 512-byte row per 128-bit load instruction); the next tile's rows are loaded
 // before the current tile's MMAs.  Split: hi/lo tf32 halves stored row-major (row stride LD = 132
@@ -434,9 +268,9 @@ __device__ __forceinline__ void split_q(const uint32_t (&q)[4], uint32_t (&h)[4]
 
 // NGF: the same Gram over the feature array n [K][ncomp][zstride] (rows = frames, columns = (component,
 // pixel) tiles of a 3-D map); the statistics slots then carry max |n| (the NGF degeneracy threshold).
-// SUP: tiles per ring stage (CTA of 8 SUP warps, warp w on tile w >> 3 of the stage): SUP = 2 runs one
-// CTA of 16 warps per SM and halves the per-CTA partials the reduction reads.
-template <bool NGF, int SUP>
+// SUP: tiles per ring stage (CTA of 8 SUP warps, warp w on tile w >> 3 of the stage); the launcher uses
+// SUP = 1 (two 8-warp CTAs per SM; one 16-warp CTA measured 15.3 vs 13.7 us at C2).
+template <bool NGF, int SUP = 1>
 __global__ void __launch_bounds__(GTM::NT * SUP, SUP == 1 ? 2 : 1) k_gram_tma(const Args a,
                                                                              const __grid_constant__ CUtensorMap vmap,
                                                                              int ntx) {
@@ -1004,177 +838,6 @@ __global__ void __launch_bounds__(P2T<D>::NT, D == 2 ? 2 : 1) k_pass2_tma(const 
         }
       }
   }
-}
-
-// Pass 2, bulk-copy pipelined (default): the same warp-level math as k_pass2_mma, but each warp streams
-// its 32-pixel blocks through two private shared-memory stages filled by 1-D bulk copies
-// (cp.async.bulk, one 128-byte row per lane: V rows, grad T rows), completion on a per-stage mbarrier;
-// the next block's rows are in flight while the current block is contracted, so no load latency is
-// exposed and no register holds in-flight data.  The epilogue reads Q and grad T from shared memory
-// and writes dD/dy with 128-bit stores.
-template <int D>
-struct P2B {
-  static constexpr int WPC = D == 2 ? 8 : 6, NT = 32 * WPC, PW = 32, LDV = 40, LDQ = 36;
-  static constexpr int VBYTES = 32 * LDV * 4, GBYTES = 32 * D * PW * 4, SBYTES = VBYTES + GBYTES;
-  static constexpr int WBYTES = 2 * SBYTES + 128;   // two stages + mbarriers
-  static constexpr int ABYTES = 2 * 2 * 4 * 32 * 16;  // M' hi / lo fragments
-  static constexpr size_t smem() { return (size_t)ABYTES + (size_t)WPC * WBYTES + 128; }
-};
-
-template <int D>
-__global__ void __launch_bounds__(P2B<D>::NT, 1) k_pass2_bulk(const Args a, const float* __restrict__ V,
-                                                             const float* __restrict__ G, long long vstride) {
-  using C = P2B<D>;
-  constexpr int LDV = C::LDV, LDQ = C::LDQ, PW = C::PW;
-  extern __shared__ __align__(128) unsigned char p2b_sh[];
-  unsigned char* base = p2b_sh + ((128 - (smem_u32(p2b_sh) & 127)) & 127);
-  float4* Ah = reinterpret_cast<float4*>(base);  // [mtile 2][kstep 4][lane 32]
-  float4* Al = Ah + 2 * 4 * 32;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  unsigned char* wb = base + C::ABYTES + (size_t)warp * C::WBYTES;
-  uint64_t* mb = reinterpret_cast<uint64_t*>(wb + 2 * C::SBYTES);
-  const int g = lane >> 2, t = lane & 3;
-  const int K = a.K;
-  const StatsLayout L(K);
-  const double* Md = a.stats + L.M;
-  for (int e = tid; e < 2 * 4 * 32; e += C::NT) {
-    const int m = e >> 7, ks = (e >> 5) & 3, ln = e & 31;
-    const int gg = ln >> 2, tt = ln & 3;
-    float hv[4], lv[4];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {  // a0 (g, t), a1 (g + 8, t), a2 (g, t + 4), a3 (g + 8, t + 4); A[j][i] = M'[i][j]
-      const int j = 16 * m + gg + 8 * (r & 1), i = 8 * ks + tt + 4 * (r >> 1);
-      const double mv = (i < K && j < K) ? Md[i * K + j] : 0.0;
-      hv[r] = to_tf32((float)mv);
-      lv[r] = (float)(mv - (double)hv[r]);
-    }
-    Ah[e] = make_float4(hv[0], hv[1], hv[2], hv[3]);
-    Al[e] = make_float4(lv[0], lv[1], lv[2], lv[3]);
-  }
-  // V rows >= K stay zero in both stages (never copied; they meet zero M' fragments, so they must be finite)
-  for (int s2 = 0; s2 < 2; ++s2) {
-    float* vz = reinterpret_cast<float*>(wb + s2 * C::SBYTES);
-    for (int e = K * LDV + lane; e < 32 * LDV; e += 32) vz[e] = 0.f;
-  }
-  if (lane == 0) {
-    mbar_init(&mb[0], 1);
-    mbar_init(&mb[1], 1);
-    fence_mbar_init();
-  }
-  fence_proxy_async_smem();
-  __syncthreads();
-  float bet[2][2];
-#pragma unroll
-  for (int m = 0; m < 2; ++m)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int j = 16 * m + g + 8 * h;
-      bet[m][h] = j < K ? (float)a.stats[L.beta + j] : 0.f;
-    }
-  // 32-bit element offsets: the launcher guarantees K D vstride and K D o_stride < 2^31, V / G rows
-  // 16-byte aligned (vstride % 4 == 0)
-  const int npix = (int)(a.pix_hi - a.pix_lo);
-  const int nblk = (npix + PW - 1) / PW;
-  const int vs = (int)vstride, os = (int)a.o_stride;
-  float* __restrict__ ob = reinterpret_cast<float*>(a.out) + (a.pix_lo - a.o_off);
-  const bool vout = ((os & 3) == 0) && (reinterpret_cast<uintptr_t>(ob) & 15) == 0;
-  const int lr = lane >> 3, lc = 4 * (lane & 7);
-  const int sg = (g & 1) ? 4 + (g >> 1) : (g >> 1);  // pixel carried by B column g
-  const int gw = blockIdx.x * C::WPC + warp, nw = gridDim.x * C::WPC;
-  const int KD = K * D;
-  auto issue = [&](int b, int s2) {
-    const int p0 = b * PW;
-    const int nb = min(PW, npix - p0);
-    const uint32_t rb = (uint32_t)(((nb + 3) & ~3) * 4);  // row bytes (reads past npix stay inside vstride)
-    float* vd = reinterpret_cast<float*>(wb + s2 * C::SBYTES);
-    float* gd = reinterpret_cast<float*>(wb + s2 * C::SBYTES + C::VBYTES);
-    if (lane == 0) mbar_arrive_expect_tx(&mb[s2], (uint32_t)(K + KD) * rb);
-    __syncwarp();
-    if (lane < K) tma_load_1d(vd + lane * LDV, V + (lane * vs + p0), rb, &mb[s2]);
-    for (int r = lane; r < KD; r += 32) tma_load_1d(gd + r * PW, G + (r * vs + p0), rb, &mb[s2]);
-  };
-  if (gw < nblk) issue(gw, 0);
-  if (gw + nw < nblk) issue(gw + nw, 1);
-  int it = 0;
-  for (int blk = gw; blk < nblk; blk += nw, ++it) {
-    const int s2 = it & 1;
-    float* Vt = reinterpret_cast<float*>(wb + s2 * C::SBYTES);
-    const float* Gt = reinterpret_cast<const float*>(wb + s2 * C::SBYTES + C::VBYTES);
-    const int p0 = blk * PW;
-    const bool fullb = p0 + PW <= npix;
-    mbar_wait(&mb[s2], (uint32_t)((it >> 1) & 1));
-    float acc[2][4][4];  // 8 independent accumulator chains
-#pragma unroll
-    for (int m = 0; m < 2; ++m)
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt) {
-        acc[m][nt][0] = acc[m][nt][1] = bet[m][0];
-        acc[m][nt][2] = acc[m][nt][3] = bet[m][1];
-      }
-#pragma unroll
-    for (int ks = 0; ks < 4; ++ks) {
-      uint32_t bh[4][2], bl[4][2];
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const float v = Vt[(8 * ks + t + 4 * u) * LDV + 8 * nt + sg];
-          const float hi = to_tf32(v);
-          bh[nt][u] = __float_as_uint(hi);
-          bl[nt][u] = __float_as_uint(v - hi);
-        }
-#pragma unroll
-      for (int m = 0; m < 2; ++m) {
-        const float4 ah = Ah[(m * 4 + ks) * 32 + lane], al = Al[(m * 4 + ks) * 32 + lane];
-        const uint32_t AH[4] = {__float_as_uint(ah.x), __float_as_uint(ah.y), __float_as_uint(ah.z),
-                                __float_as_uint(ah.w)};
-        const uint32_t AL[4] = {__float_as_uint(al.x), __float_as_uint(al.y), __float_as_uint(al.z),
-                                __float_as_uint(al.w)};
-        // one product at a time over the n-tiles: consecutive HMMAs hit independent accumulators
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt) mma_tf32(acc[m][nt], AH, bh[nt][0], bh[nt][1]);
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt) mma_tf32(acc[m][nt], AL, bh[nt][0], bh[nt][1]);
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt) mma_tf32(acc[m][nt], AH, bl[nt][0], bl[nt][1]);
-      }
-    }
-    __syncwarp();  // every lane's V reads are done before Q overwrites the tile
-    const uint32_t sq = smem_u32(Vt) + (uint32_t)((((lane & 7) + 8 * (lane >> 4)) * LDQ + 4 * ((lane >> 3) & 1)) * 4);
-#pragma unroll
-    for (int m = 0; m < 2; ++m)
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt)
-        stsm_x4(sq + (uint32_t)((16 * m * LDQ + 8 * nt) * 4), acc[m][nt][0], acc[m][nt][1], acc[m][nt][2],
-                acc[m][nt][3]);
-    __syncwarp();
-    // epilogue: dD/dy_j,c(p) = Q[j][p] grad T_j,c(p), rows j = 4 q + lr, pixels p0 + lc .. + 3
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int j = 4 * q + lr, c = p0 + lc;
-      if (j < K) {
-        const float4 qv = *reinterpret_cast<const float4*>(Vt + j * LDQ + lc);
-#pragma unroll
-        for (int cc = 0; cc < D; ++cc) {
-          const float4 gv = *reinterpret_cast<const float4*>(Gt + (j * D + cc) * PW + lc);
-          const float4 r = make_float4(qv.x * gv.x, qv.y * gv.y, qv.z * gv.z, qv.w * gv.w);
-          float* dst = ob + ((j * D + cc) * os + c);
-          if (fullb && vout) {
-            __stcs(reinterpret_cast<float4*>(dst), r);
-          } else {
-            if (c < npix) __stcs(dst, r.x);
-            if (c + 1 < npix) __stcs(dst + 1, r.y);
-            if (c + 2 < npix) __stcs(dst + 2, r.z);
-            if (c + 3 < npix) __stcs(dst + 3, r.w);
-          }
-        }
-      }
-    }
-    __syncwarp();              // Q / grad T reads done before the stage is refilled
-    fence_proxy_async_smem();  // generic accesses of the stage before the async-proxy writes
-    if (blk + 2 * nw < nblk) issue(blk + 2 * nw, s2);
-  }
-  // drain: no copies may be in flight when the CTA exits (every issued stage was waited on above)
 }
 
 // Split NGF pass 2, z = dD/d(grad u) on the tensor cores (fp32 displacement fields, K <= 128):

@@ -217,15 +217,21 @@ __global__ void __maxnreg__(96) k_ngf_z_tc(const Args a, const float* __restrict
         const int u = wq + C::WPQ * m, mt = u / nfg, fg = u % nfg;
         const int p = (int)(t * TP) + mt * PXT + PXW * qb + pxl;
         const bool ok = lane_ok && p < nzp;
-        const float* nb = Nf + ((unsigned)c * zsu + (ok ? (unsigned)p : 0u));
-        const unsigned o = (unsigned)(8 * fg);
+        // running pointer over the unit's 8 frames (one 64-bit add per load)
+        const float* np = Nf + ((unsigned)c * zsu + (ok ? (unsigned)p : 0u)) + (size_t)(8 * fg) * sn;
         if (u < nun) {
           if (8 * fg + 8 <= K) {
 #pragma unroll
-            for (int v = 0; v < 8; ++v) x[m][v] = ok ? __ldg(nb + (o + v) * sn) : 0.f;
+            for (int v = 0; v < 8; ++v) {
+              x[m][v] = ok ? __ldg(np) : 0.f;
+              np += sn;
+            }
           } else {
 #pragma unroll
-            for (int v = 0; v < 8; ++v) x[m][v] = (ok && 8 * fg + v < K) ? __ldg(nb + (o + v) * sn) : 0.f;
+            for (int v = 0; v < 8; ++v) {
+              x[m][v] = (ok && 8 * fg + v < K) ? __ldg(np) : 0.f;
+              np += sn;
+            }
           }
         }
       }
@@ -333,14 +339,19 @@ __global__ void __maxnreg__(96) k_ngf_z_tc(const Args a, const float* __restrict
           zz[jj] = (r - nv[jj] * dot) * ir[jj];
         }
         if (ok) {
-          const unsigned o = (unsigned)(ch * 8);
+          float* zp = zb + (size_t)(ch * 8) * sn;  // running pointer over the chunk's 8 frames
           if (ch * 8 + 8 <= K) {
 #pragma unroll
-            for (int jj = 0; jj < 8; ++jj) zb[(o + jj) * sn] = zz[jj];
+            for (int jj = 0; jj < 8; ++jj) {
+              *zp = zz[jj];
+              zp += sn;
+            }
           } else {
 #pragma unroll
-            for (int jj = 0; jj < 8; ++jj)
-              if (ch * 8 + jj < K) zb[(o + jj) * sn] = zz[jj];
+            for (int jj = 0; jj < 8; ++jj) {
+              if (ch * 8 + jj < K) *zp = zz[jj];
+              zp += sn;
+            }
           }
         }
       }
@@ -354,7 +365,7 @@ __global__ void __maxnreg__(96) k_ngf_z_tc(const Args a, const float* __restrict
       const uint32_t idesc = umma_idesc_f16(128, KN);
       for (long long n = 0; n < nloc; ++n) {
         const int s = (int)(n % NST);
-        mbar_wait(&a_full[s], (uint32_t)((n / NST) & 1));
+        mbar_wait_sleep(&a_full[s], (uint32_t)((n / NST) & 1));
         tc_fence_after();
         const uint32_t bh0 = smem_u32(Bh), bl0 = smem_u32(Bl);
         for (int mt = 0; mt < MT; ++mt)

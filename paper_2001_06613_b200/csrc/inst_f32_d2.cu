@@ -2,10 +2,6 @@
 #include "launch.cuh"
 namespace sr {
 SR_DEFINE_INST(f32, float, 2)
-cudaError_t pass1_split_d2(const Launch& L, const Args& a, float* V, float* G, long long vstride, double* part,
-                           size_t cap, int* nblk) {
-  return run_pass1_split<2>(L, a, V, G, vstride, part, cap, nblk);
-}
 cudaError_t pass2_stream_d2(const Launch& L, const Args& a, const float* V, const float* G, long long vstride) {
   return run_pass2_stream<2>(L, a, V, G, vstride);
 }

@@ -48,10 +48,7 @@ struct Launch {
   int sms;
   int grid_override;  // 0 = auto
   int legacy;         // 1 = force the non-specialized kernels (A/B checks)
-  int ws2;            // 1 = warp-specialized pass 2 (experimental)
-  int tc;             // 1 = tcgen05 Gram in pass 1 (fp32 NCC displacement, K <= 32)
-  int split;          // 1 = split pass 1 (sampling kernel + tensor-core Gram kernel; default)
-  int tc2;            // 1 = tcgen05 pass 2 (2-D fp32 NCC displacement; slower than the SIMT pass 2 today)
+  int tc;             // 0 = no tensor-core split pass 1 (SIMT Gram k_pass1_ws for fp32 NCC, K <= 32)
 };
 
 template <typename K>
@@ -71,9 +68,6 @@ struct Runner {
   // pass 1; per-CTA partials [grid][KP*KP + 3KP] in `part`, CTA count in *nblk
   static cudaError_t pass1(const Launch& L, const Args& a, double* part, size_t part_cap,
                            int* nblk) {
-    if constexpr (std::is_same<T, float>::value && FEAT == NCC && PARAM == DISP && KP == 32) {
-      if (!L.legacy && L.tc) return pass1_tc(L, a, part, part_cap, nblk);
-    }
     if constexpr (FEAT == NCC && PARAM == DISP && KP <= 32) {
       if (!L.legacy) return pass1_ws(L, a, part, part_cap, nblk);
     }
@@ -95,30 +89,6 @@ struct Runner {
     return cudaGetLastError();
   }
 
-  // pass 1 with the Gram on tcgen05 tensor cores (fp32 NCC displacement, K <= 32), engine_tc.cuh
-  static cudaError_t pass1_tc(const Launch& L, const Args& a, double* part, size_t part_cap, int* nblk) {
-    using C = TC1<D>;
-    const size_t smem = tc1_smem<D>();
-    auto kern = k_pass1_tc<D>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    const long long npix = a.pix_hi - a.pix_lo;
-    const long long ntiles = (npix + C::TP - 1) / C::TP;
-    int grid = L.sms;  // one CTA per SM (TMEM, 1 CTA/SM by shared memory)
-    if (L.grid_override > 0) grid = L.grid_override;
-    if (grid > ntiles) grid = (int)(ntiles > 0 ? ntiles : 1);
-    const size_t stride = (size_t)C::KP * C::KP + 3 * C::KP;
-    if ((size_t)grid * stride > part_cap) grid = (int)(part_cap / stride);
-    Args b = a;
-    b.part = part;
-    CUtensorMap ymap;
-    memset(&ymap, 0, sizeof ymap);
-    b.ymap_ok = encode_y_map<float>(&ymap, a, a.K * D, C::TP) ? 1 : 0;
-    kern<<<grid, C::NT, smem, L.stream>>>(b, ymap);
-    *nblk = grid;
-    return cudaGetLastError();
-  }
-
   // warp-specialized pass 1 (NCC displacement, KP <= 32), engine_ws.cuh
   static cudaError_t pass1_ws(const Launch& L, const Args& a, double* part, size_t part_cap, int* nblk) {
     using C = WS1<T, KP>;
@@ -136,59 +106,13 @@ struct Runner {
     CUtensorMap ymap;
     memset(&ymap, 0, sizeof ymap);
     b.ymap_ok = encode_y_map<T>(&ymap, a, a.K * D, C::TP) ? 1 : 0;
-    if (getenv("SEQREG_B200_TRACE"))
-      fprintf(stderr, "[seqreg_b200] pass1_ws grid=%d smem=%zu dbg=%d ymap_ok=%d\n", grid, smem, b.dbg, b.ymap_ok);
     kern<<<grid, C::NT, smem, L.stream>>>(b, ymap);
     *nblk = grid;
     return cudaGetLastError();
   }
 
-  // warp-specialized pass 2 (NCC displacement, KP <= 32), engine_ws.cuh
-  static cudaError_t pass2_ws(const Launch& L, const Args& a, int* nblk_out) {
-    using C = WS2<T, KP>;
-    const size_t smem = ws2_smem<T, D, KP>();
-    auto kern = k_pass2_ws<T, D, KP>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    const long long npix = a.pix_hi - a.pix_lo;
-    const long long ntiles = (npix + C::TP - 1) / C::TP;
-    int grid = occupancy_grid(L, kern, C::NT, smem, ntiles > 0 ? ntiles : 1);
-    Args b = a;
-    CUtensorMap ymap;
-    memset(&ymap, 0, sizeof ymap);
-    b.ymap_ok = encode_y_map<T>(&ymap, a, a.K * D, C::TP) ? 1 : 0;
-    kern<<<grid, C::NT, smem, L.stream>>>(b, ymap);
-    *nblk_out = grid;
-    return cudaGetLastError();
-  }
-
-  // pass 2 with the coefficient contraction on tcgen05 (fp32 NCC displacement, 2-D, K <= 32)
-  static cudaError_t pass2_tc(const Launch& L, const Args& a, int* nblk_out) {
-    using C = TC2;
-    const size_t smem = tc2_smem();
-    cudaError_t e = cudaFuncSetAttribute(k_pass2_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    const long long npix = a.pix_hi - a.pix_lo;
-    const long long ntiles = (npix + C::TP - 1) / C::TP;
-    int grid = L.grid_override > 0 ? L.grid_override : L.sms;
-    if (grid > ntiles) grid = (int)(ntiles > 0 ? ntiles : 1);
-    Args b = a;
-    CUtensorMap ymap;
-    memset(&ymap, 0, sizeof ymap);
-    b.ymap_ok = encode_y_map<float>(&ymap, a, a.K * 2, C::TP) ? 1 : 0;
-    k_pass2_tc<<<grid, C::NT, smem, L.stream>>>(b, ymap);
-    *nblk_out = grid;
-    return cudaGetLastError();
-  }
-
   static cudaError_t pass2(const Launch& L, const Args& a, double* part_aff, size_t aff_cap,
                            int* nblk_out) {
-    if constexpr (std::is_same<T, float>::value && FEAT == NCC && PARAM == DISP && KP <= 32 && D == 2) {
-      if (!L.legacy && L.tc2) return pass2_tc(L, a, nblk_out);
-    }
-    if constexpr (FEAT == NCC && PARAM == DISP && KP <= 32) {
-      if (!L.legacy && L.ws2) return pass2_ws(L, a, nblk_out);
-    }
     using C = G2<T, KP>;
     constexpr int NA = D * (D + 1);
     size_t smem = pass2_smem<T, D, FEAT, KP>();
@@ -239,51 +163,6 @@ cudaError_t run_curvature(const Launch& L, const Args& a, double alpha, double h
   return cudaGetLastError();
 }
 
-// Split pass 1 for fp32 NCC displacement (K <= 32): k_sample_v (V = v - shift, [K][vstride])
-// then k_gram_tc (TMA V tiles -> hi/lo SW128 tiles -> tcgen05 Gram).  engine_tc.cuh.
-template <int D>
-cudaError_t run_pass1_split(const Launch& L, const Args& a, float* V, float* G, long long vstride, double* part,
-                            size_t part_cap, int* nblk) {
-  const long long npix = a.pix_hi - a.pix_lo;
-  if (npix <= 0) return cudaErrorInvalidValue;
-  constexpr int SPT = 4;
-  const long long per_frame = (npix + 256 * SPT - 1) / (256 * SPT);
-  const dim3 sgrid((unsigned)per_frame, (unsigned)a.K);
-  if (G) {
-    if (a.g.pow2) k_sample_v<D, true, SPT, true><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
-    else k_sample_v<D, false, SPT, true><<<sgrid, 256, 0, L.stream>>>(a, V, G, vstride);
-  } else {
-    if (a.g.pow2) k_sample_v<D, true, SPT, false><<<sgrid, 256, 0, L.stream>>>(a, V, nullptr, vstride);
-    else k_sample_v<D, false, SPT, false><<<sgrid, 256, 0, L.stream>>>(a, V, nullptr, vstride);
-  }
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  EncodeTiledFn fn = encode_tiled_fn();
-  if (!fn) return cudaErrorNotSupported;
-  CUtensorMap vmap;
-  memset(&vmap, 0, sizeof vmap);
-  cuuint64_t gdim[2] = {(cuuint64_t)npix, (cuuint64_t)a.K};
-  cuuint64_t gstr[1] = {(cuuint64_t)vstride * 4};
-  cuuint32_t box[2] = {(cuuint32_t)TCG::TP, (cuuint32_t)TCG::KP};
-  cuuint32_t es[2] = {1, 1};
-  if (fn(&vmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, V, gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
-      CUDA_SUCCESS)
-    return cudaErrorInvalidValue;
-  const size_t smem = tcg_smem();
-  e = cudaFuncSetAttribute(k_gram_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  const long long ntiles = (npix + TCG::TP - 1) / TCG::TP;
-  int grid = L.grid_override > 0 ? L.grid_override : L.sms;
-  if (grid > ntiles) grid = (int)ntiles;
-  const size_t stride = (size_t)TCG::KP * TCG::KP + 3 * TCG::KP;
-  if ((size_t)grid * stride > part_cap) grid = (int)(part_cap / stride);
-  Args b = a;
-  b.part = part;
-  k_gram_tc<<<grid, TCG::NT, smem, L.stream>>>(b, vmap);
-  *nblk = grid;
-  return cudaGetLastError();
-}
 // Split NGF path (engine_ngf.cuh).  Ranges: V / grad T over [vlo, vhi) = slab +- 2 rows, n / rho / z over
 // [zlo, zhi) = slab +- 1 row, the Gram over the slab.  cudaErrorNotSupported: layouts the TMA map cannot
 // express (the caller falls back to the generic kernels).
@@ -400,10 +279,6 @@ cudaError_t ngf_pass1_d3(const Launch& L, const Args& a, const NgfBufs& B, doubl
 cudaError_t ngf_pass2_d2(const Launch& L, const Args& a, const NgfBufs& B);
 cudaError_t ngf_pass2_d3(const Launch& L, const Args& a, const NgfBufs& B);
 
-cudaError_t pass1_split_d2(const Launch& L, const Args& a, float* V, float* G, long long vstride, double* part,
-                           size_t cap, int* nblk);
-cudaError_t pass1_split_d3(const Launch& L, const Args& a, float* V, float* G, long long vstride, double* part,
-                           size_t cap, int* nblk);
 template <int D>
 cudaError_t run_pass2_stream(const Launch& L, const Args& a, const float* V, const float* G, long long vstride) {
   const long long npix = a.pix_hi - a.pix_lo;
@@ -412,11 +287,7 @@ cudaError_t run_pass2_stream(const Launch& L, const Args& a, const float* V, con
   return cudaGetLastError();
 }
 cudaError_t pass2_stream_d2(const Launch& L, const Args& a, const float* V, const float* G, long long vstride);
-// engine_mma.cuh (mma_pass.cu): fused sampling + mma.sync Gram pass 1, mma.sync streaming pass 2
-cudaError_t sample_gram_d2(const Launch& L, const Args& a, float* V, float* G, long long vstride, double* part,
-                           size_t cap, int* nblk);
-cudaError_t sample_gram_d3(const Launch& L, const Args& a, float* V, float* G, long long vstride, double* part,
-                           size_t cap, int* nblk);
+// engine_mma.cuh (mma_pass.cu): sampling + TMA-fed mma.sync Gram pass 1, mma.sync streaming pass 2
 cudaError_t sample_then_gram_d2(const Launch& L, const Args& a, float* V, float* G, long long vstride, double* part,
                                 size_t cap, int* nblk);
 cudaError_t sample_then_gram_d3(const Launch& L, const Args& a, float* V, float* G, long long vstride, double* part,

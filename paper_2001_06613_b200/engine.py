@@ -169,18 +169,6 @@ class DeviceFrames:
         check(engine.lib.sr_frame_shifts(engine.ctx, DTYPES[data.dtype], ctypes.c_void_p(self.data.data_ptr()),
                                          int(data.shape[0]), int(data.shape[1]),
                                          ctypes.c_void_p(self.shifts.data_ptr())))
-        # fp32 stacks: gather-capable array copy for the texture sampling path (sr_frames_prepare)
-        self._grid_c = grid.c_struct()
-        check(engine.lib.sr_frames_prepare(engine.ctx, DTYPES[data.dtype], ctypes.c_void_p(self.data.data_ptr()),
-                                           int(data.shape[0]), ctypes.byref(self._grid_c)))
-        self._prepared = True
-
-    def __del__(self):
-        try:
-            if getattr(self, "_prepared", False) and self.engine.ctx is not None:
-                self.engine.lib.sr_frames_release(self.engine.ctx, ctypes.c_void_p(self.data.data_ptr()))
-        except Exception:
-            pass
 
     @classmethod
     def from_array(cls, engine: Engine, values, grid: GridSpec, dtype: torch.dtype) -> "DeviceFrames":
