@@ -68,7 +68,9 @@ extern "C" {
 #define SR_ERR_UNSUPPORTED 4 /* e.g. more than SR_MAX_FRAMES subset frames */
 #define SR_ERR_CALLBACK 5    /* a caller-supplied callback returned non-zero (its error is the caller's) */
 
-#define SR_MAX_FRAMES 128    /* subset size limit of the fused kernels */
+#define SR_MAX_FRAMES 160    /* subset size limit: the kernels see <= 128 frames, larger subsets run as
+                                blocks of 64 frames (two per launch); the K x K finalize of a subset must
+                                fit in shared memory */
 
 /* dtype */
 #define SR_F32 0

@@ -43,7 +43,7 @@ SR_OK, SR_ERR_ARG, SR_ERR_CUDA, SR_ERR_SINGULAR, SR_ERR_UNSUPPORTED, SR_ERR_CALL
 SR_F32, SR_F64 = 0, 1
 SR_NCC, SR_NGF = 0, 1
 SR_AFFINE, SR_DISPLACEMENT = 0, 1
-SR_MAX_FRAMES = 128
+SR_MAX_FRAMES = 160
 
 _LIBNAME = "libseqreg_b200.so"
 

@@ -86,6 +86,15 @@ struct sr_ctx {
   double* curv_s = nullptr;
   double* curv_part = nullptr;
   size_t curv_part_cap = 0;
+  // subsets of more than kBlockMax frames: one sub-problem's raw sums, stats, fields and gradient rows
+  double* lraw = nullptr;
+  size_t lraw_cap = 0;
+  double* lstats = nullptr;
+  size_t lstats_cap = 0;
+  void* ly = nullptr;
+  size_t ly_bytes = 0;
+  void* lgrad = nullptr;
+  size_t lgrad_bytes = 0;
   int* iaux = nullptr;
   size_t iaux_cap = 0;
 };
@@ -504,6 +513,10 @@ int sr_destroy(sr_ctx* c) {
   cudaFree(c->part);
   cudaFree(c->ticket);
   cudaFree(c->curv_part);
+  cudaFree(c->lraw);
+  cudaFree(c->lstats);
+  cudaFree(c->ly);
+  cudaFree(c->lgrad);
   if (c->order_ev) cudaEventDestroy(c->order_ev);
   sr::lbfgs::destroy(c->lbfgs);
   cudaFree(c->vbuf);
@@ -567,11 +580,139 @@ int sr_frame_shifts(sr_ctx* c, int32_t dtype, const void* frames, int32_t nframe
   return SR_OK;
 }
 
+}  // extern "C"
+
+// ---------------------------------------------------------------- subsets of more than kBlockMax frames
+// (ADVICE: the paper's schedule build_temporal_levels(129, 17) ends with a 129-frame level.)  The subset is
+// cut into blocks of kBlockFrames; pass 1 runs once per pair of blocks (<= 128 frames per launch) and its
+// raw sums are scattered into the K x K ones; the finalize runs on all K frames; pass 2 runs once per
+// (input block, output block) with the gradient coefficients restricted to that block pair (k_sub_stats) and
+// the output rows accumulated into the gradient (k_acc_rows).  Each kernel is unchanged, so the results are
+// the single-launch arithmetic up to the order of the pass-2 sums over input blocks.
+static constexpr int kBlockFrames = 64;
+
+static SubIdx sub_blocks(int K, int bi, int bj) {  // frames of block bi (then block bj when different)
+  SubIdx s{};
+  auto add = [&](int b, unsigned char part) {
+    for (int f = b * kBlockFrames; f < std::min(K, (b + 1) * kBlockFrames); ++f) {
+      s.idx[s.n] = f;
+      s.part[s.n] = part;
+      ++s.n;
+    }
+  };
+  if (bi == bj) {
+    add(bi, 2);
+  } else {
+    add(bi, 0);
+    add(bj, 1);
+  }
+  return s;
+}
+
+struct SubProblem {
+  sr_problem q;
+  std::vector<int32_t> fi;
+  std::vector<double> aff;
+};
+
+// the sub-problem of frames s.idx (the displacement fields gathered into ctx->ly)
+static int make_sub(sr_ctx* c, const sr_problem* p, const SubIdx& s, SubProblem& sp) {
+  sp.q = *p;
+  sp.q.k = s.n;
+  sp.fi.resize(s.n);
+  for (int i = 0; i < s.n; ++i) sp.fi[i] = p->frame_index[s.idx[i]];
+  sp.q.frame_index = sp.fi.data();
+  const int d = p->grid.ndim;
+  if (p->param == SR_AFFINE) {
+    const int na = d * d + d;
+    sp.aff.resize((size_t)s.n * na);
+    for (int i = 0; i < s.n; ++i)
+      for (int e = 0; e < na; ++e) sp.aff[(size_t)i * na + e] = p->affine[(size_t)s.idx[i] * na + e];
+    sp.q.affine = sp.aff.data();
+    return SR_OK;
+  }
+  const size_t esz = p->dtype == SR_F32 ? 4 : 8;
+  const long long row = (long long)d * p->y_stride;
+  int rc = ensure(&c->ly, &c->ly_bytes, (size_t)kBlockMax * row * esz);
+  if (rc) return rc;
+  const dim3 grid((unsigned)std::min<long long>((row + 255) / 256, 4096), (unsigned)s.n);
+  if (p->dtype == SR_F32)
+    k_gather_rows<float><<<grid, 256, 0, c->stream>>>((const float*)p->y_dev, row, s, (float*)c->ly);
+  else
+    k_gather_rows<double><<<grid, 256, 0, c->stream>>>((const double*)p->y_dev, row, s, (double*)c->ly);
+  CK(cudaGetLastError());
+  sp.q.y_dev = c->ly;
+  return SR_OK;
+}
+
+static int corr_partial_large(sr_ctx* c, const sr_problem* p, double* raw) {
+  const int K = p->k, nb = (K + kBlockFrames - 1) / kBlockFrames;
+  CK(cudaMemsetAsync(raw, 0, sizeof(double) * (size_t)sr_raw_size(K), c->stream));
+  int rc = ensure_d(&c->lraw, &c->lraw_cap, (size_t)sr_raw_size(kBlockMax));
+  if (rc) return rc;
+  for (int bi = 0; bi < nb; ++bi)
+    for (int bj = bi + 1; bj < nb; ++bj) {
+      const SubIdx s = sub_blocks(K, bi, bj);
+      SubProblem sp;
+      rc = make_sub(c, p, s, sp);
+      if (rc) return rc;
+      rc = upload_job(c, &sp.q, nullptr);
+      if (rc) return rc;
+      rc = corr_partial_impl(c, &sp.q, c->lraw);
+      if (rc) return rc;
+      k_scatter_raw<<<64, 256, 0, c->stream>>>(c->lraw, s, K, raw);
+      CK(cudaGetLastError());
+    }
+  c->vtag.valid = 0;  // the split paths' samples belong to the last sub-problem
+  return SR_OK;
+}
+
+extern "C" {  // (defined below, inside the boundary's extern "C" block)
+static int grad_impl_core(sr_ctx* c, const sr_problem* p, const double* stats, void* grad, int64_t g_off,
+                          int64_t g_stride, bool reuse, bool* curv_done);
+}
+
+static int grad_large(sr_ctx* c, const sr_problem* p, const double* stats, void* grad, int64_t g_off,
+                      int64_t g_stride) {
+  const int K = p->k, nb = (K + kBlockFrames - 1) / kBlockFrames, d = p->grid.ndim;
+  const bool aff = p->param == SR_AFFINE;
+  const size_t esz = aff ? 8 : (p->dtype == SR_F32 ? 4 : 8);
+  const long long row = aff ? d * d + d : (long long)d * g_stride;
+  int rc = ensure_d(&c->lstats, &c->lstats_cap, (size_t)StatsLayout(kBlockMax).total);
+  if (rc) return rc;
+  rc = ensure(&c->lgrad, &c->lgrad_bytes, (size_t)kBlockMax * row * esz);
+  if (rc) return rc;
+  for (int bj = 0; bj < nb; ++bj)
+    for (int bi = 0; bi < nb; ++bi) {
+      const SubIdx s = sub_blocks(K, bi, bj);
+      SubProblem sp;
+      rc = make_sub(c, p, s, sp);
+      if (rc) return rc;
+      rc = upload_job(c, &sp.q, nullptr);
+      if (rc) return rc;
+      k_sub_stats<<<64, 256, 0, c->stream>>>(stats, K, s, bi == 0 ? 1 : 0, c->lstats);
+      CK(cudaGetLastError());
+      bool done = false;
+      rc = grad_impl_core(c, &sp.q, c->lstats, c->lgrad, g_off, g_stride, false, &done);
+      if (rc) return rc;
+      const dim3 grid((unsigned)std::min<long long>((row + 255) / 256, 4096), (unsigned)s.n);
+      if (esz == 4)
+        k_acc_rows<float><<<grid, 256, 0, c->stream>>>((const float*)c->lgrad, row, s, bi == 0, (float*)grad);
+      else
+        k_acc_rows<double><<<grid, 256, 0, c->stream>>>((const double*)c->lgrad, row, s, bi == 0, (double*)grad);
+      CK(cudaGetLastError());
+    }
+  return SR_OK;
+}
+
+extern "C" {
+
 int sr_corr_partial(sr_ctx* c, const sr_problem* p, double* raw_dev) {
   int rc = check_problem(c, p);
   if (rc) return rc;
   if (!raw_dev) return fail(SR_ERR_ARG, "raw_dev is null");
   CK(cudaSetDevice(c->device));
+  if (p->k > kBlockMax) return corr_partial_large(c, p, raw_dev);
   rc = upload_job(c, p, nullptr);
   if (rc) return rc;
   return corr_partial_impl(c, p, raw_dev);
@@ -695,6 +836,7 @@ int sr_grad(sr_ctx* c, const sr_problem* p, const double* stats_dev, void* grad_
   if (!stats_dev || !grad_dev) return fail(SR_ERR_ARG, "null stats/grad");
   if (p->param == SR_DISPLACEMENT && g_stride < 1) return fail(SR_ERR_ARG, "g_stride must be >= 1");
   CK(cudaSetDevice(c->device));
+  if (p->k > kBlockMax) return grad_large(c, p, stats_dev, grad_dev, g_off, g_stride);
   rc = upload_job(c, p, nullptr);
   if (rc) return rc;
   return grad_impl(c, p, stats_dev, grad_dev, g_off, g_stride, c->sample_reuse != 0);
@@ -768,6 +910,19 @@ int sr_evaluate(sr_ctx* c, const sr_problem* p, const double* weights, double ce
   const Geo g = make_geo(p->grid);
   if (p->pix_lo != 0 || p->pix_hi != g.N) return fail(SR_ERR_ARG, "sr_evaluate covers the whole grid");
   CK(cudaSetDevice(c->device));
+  if (p->k > kBlockMax) {  // frame blocks (no graph replay)
+    rc = corr_partial_large(c, p, raw_dev);
+    if (rc) return rc;
+    rc = upload_job(c, p, weights);
+    if (rc) return rc;
+    rc = finalize_impl(c, p, raw_dev, cell_volume, g.N, stats_dev);
+    if (rc || !grad_dev) return rc;
+    rc = grad_large(c, p, stats_dev, grad_dev, p->y_off, p->param == SR_DISPLACEMENT ? p->y_stride : 0);
+    if (rc) return rc;
+    if (c->curv_alpha > 0 && p->param == SR_DISPLACEMENT)
+      return curvature_impl(c, p, c->curv_alpha, c->curv_h, grad_dev, p->y_off, p->y_stride, c->curv_s);
+    return SR_OK;
+  }
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   CK(cudaStreamIsCapturing(c->stream, &cs));
   if (!c->graphs || cs != cudaStreamCaptureStatusNone) {  // (the caller may be capturing)

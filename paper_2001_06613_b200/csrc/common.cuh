@@ -16,7 +16,8 @@
 
 namespace sr {
 
-constexpr int kMaxFrames = 128;
+constexpr int kMaxFrames = 256;  // subset size limit (SR_MAX_FRAMES); the kernels see at most 128 (kBlockMax)
+constexpr int kBlockMax = 128;   // frames per kernel launch: larger subsets run as frame blocks (capi.cu)
 
 // Grid geometry passed by value to every kernel.
 struct Geo {

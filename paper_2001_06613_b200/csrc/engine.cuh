@@ -1216,6 +1216,77 @@ __device__ __forceinline__ double lap_u(const Args& a, const T* __restrict__ yc,
   return out;
 }
 
+// ---- subsets of more than kBlockMax frames (capi.cu, large-K path): the problem runs as sub-problems of
+// at most kBlockMax frames (pairs of frame blocks); these kernels move rows between the full problem and a
+// sub-problem.  SubIdx: sub-problem position i <-> subset position idx[i]; part[i] = 0 input block only,
+// 1 output block only, 2 both.
+struct SubIdx {
+  int n;
+  int idx[kBlockMax];
+  unsigned char part[kBlockMax];
+};
+
+// scatter a sub-problem's raw sums [G n^2 | s n | vmax n | -vmin n | count] into the full raw sums
+static __global__ void __launch_bounds__(256) k_scatter_raw(const double* __restrict__ sub, const SubIdx s, int K,
+                                                     double* __restrict__ raw) {
+  const int n = s.n;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n * n + 3 * n + 1; e += gridDim.x * blockDim.x) {
+    if (e < n * n) {
+      raw[(long long)s.idx[e / n] * K + s.idx[e % n]] = sub[e];
+    } else if (e < n * n + 3 * n) {
+      const int f = (e - n * n) / n, i = (e - n * n) % n;
+      raw[(long long)K * K + (long long)f * K + s.idx[i]] = sub[e];
+    } else {
+      raw[(long long)K * K + 3LL * K] = sub[e];
+    }
+  }
+}
+
+// the gradient coefficients of a sub-problem: M'_sub[i][j] = M'[idx_i][idx_j] for an input frame i and an
+// output frame j (else 0), beta'_sub[j] = beta'[idx_j] for an output frame when add_beta (the first input
+// block of this output block), in the sub-problem's stats layout (fp64 M, fp32 copy Mf, beta)
+static __global__ void __launch_bounds__(256) k_sub_stats(const double* __restrict__ stats, int K, const SubIdx s,
+                                                   int add_beta, double* __restrict__ sub) {
+  const StatsLayout L(K), Ls(s.n);
+  const int n = s.n;
+  float* mf = reinterpret_cast<float*>(sub + Ls.Mf);
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n * n + n; e += gridDim.x * blockDim.x) {
+    if (e < n * n) {
+      const int i = e / n, j = e % n;
+      const double v = (s.part[i] != 1 && s.part[j] != 0) ? stats[L.M + (long long)s.idx[i] * K + s.idx[j]] : 0.0;
+      sub[Ls.M + e] = v;
+      mf[e] = (float)v;
+    } else {
+      const int j = e - n * n;
+      sub[Ls.beta + j] = (add_beta && s.part[j] != 0) ? stats[L.beta + s.idx[j]] : 0.0;
+    }
+  }
+}
+
+// rows of the sub-problem's output frames into the full gradient (first: copy, else add); rows of row_len
+// elements ([d][g_stride] for displacement fields, the d*d + d affine parameters)
+template <typename T>
+__global__ void __launch_bounds__(256) k_acc_rows(const T* __restrict__ tmp, long long row_len, const SubIdx s,
+                                                  int first, T* __restrict__ grad) {
+  const int j = blockIdx.y;
+  if (s.part[j] == 0) return;
+  const T* src = tmp + (long long)j * row_len;
+  T* dst = grad + (long long)s.idx[j] * row_len;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < row_len; e += (long long)gridDim.x * blockDim.x)
+    dst[e] = first ? src[e] : dst[e] + src[e];
+}
+
+// gather rows: out[i] = src[idx_i] (the sub-problem's displacement fields)
+template <typename T>
+__global__ void __launch_bounds__(256) k_gather_rows(const T* __restrict__ src, long long row_len, const SubIdx s,
+                                                     T* __restrict__ out) {
+  const int i = blockIdx.y;
+  const T* a = src + (long long)s.idx[i] * row_len;
+  T* b = out + (long long)i * row_len;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < row_len; e += (long long)gridDim.x * blockDim.x)
+    b[e] = a[e];
+}
+
 // T_j(y_j(x)) for every subset frame j and pixel of [pix_lo, pix_hi): out[j][pix - pix_lo] (sr_sample; the
 // warped values behind CorrelationState.features, similarity.py:143-150)
 template <typename T, int D, int PARAM>
