@@ -1,0 +1,23 @@
+#!/bin/bash
+# GPU box: the round's profiles (run after the code is final for the round).
+#   per config: DRAM bytes + device time of every engine kernel of one evaluation (cold L2) -> traffic JSON;
+#   the bench launch list (gpu__time_duration, --clock-control none) for C3;
+#   one --set full capture of each C3 kernel and of the C2 / C4 top kernels.
+set -u
+out=${1:-gpurun_out/prof}
+mkdir -p "$out"
+for c in c3 c4 c2; do
+  timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    -k regex:"^k_" -o "$out/tr_$c" python scripts/evalloop.py --config $c --reps 1 > "$out/tr_$c.log" 2>&1
+done
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"^k_" -c 400 --csv \
+  --log-file "$out/launches_c3.csv" python bench.py --steps 2 --warmup 1 --only --no-cpu > "$out/launches_c3.log" 2>&1
+for k in k_ngf_sfeat2 k_gram_tcx k_ngf_z_tc k_ngf_adj4; do
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:"^$k" -c 1 -o "$out/full_c3_$k" \
+    python scripts/evalloop.py --config c3 --reps 1 > /dev/null 2>&1
+done
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"^k_sample_vp" -c 1 -o "$out/full_c2_k_sample_vp" \
+  python scripts/evalloop.py --config c2 --reps 1 > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"^k_ngf_z_f16" -c 1 -o "$out/full_c4_k_ngf_z_f16" \
+  python scripts/evalloop.py --config c4 --reps 1 > /dev/null 2>&1
+ls -la "$out"
