@@ -21,3 +21,15 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:"^k_
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"^k_ngf_z_f16" -c 1 -o "$out/full_c4_k_ngf_z_f16" \
   python scripts/evalloop.py --config c4 --reps 1 > /dev/null 2>&1
 ls -la "$out"
+# summaries on the box (the .ncu-rep files are large); keep only the small full-set reps
+for c in c3 c4 c2; do
+  python scripts/summarize_ncu.py --rep "$out/tr_$c.ncu-rep" --out "$out/tr_$c.txt" --traffic-out "$out/traffic_$c.json" > /dev/null 2>&1
+done
+python scripts/summarize_ncu.py --launches "$out/launches_c3.csv" --out "$out/launches_c3.txt" > /dev/null 2>&1
+for f in "$out"/full_*.ncu-rep; do
+  python scripts/summarize_ncu.py --rep "$f" --out "${f%.ncu-rep}.txt" > /dev/null 2>&1
+  ncu -i "$f" --page source --csv --print-source sass > "${f%.ncu-rep}.sass.csv" 2>/dev/null
+done
+rm -f "$out"/tr_*.ncu-rep
+for f in "$out"/full_*.ncu-rep; do [ "$(stat -c %s "$f")" -gt 8000000 ] && rm -f "$f"; done
+du -sh "$out"
