@@ -412,8 +412,8 @@ def test_single_frame_and_bad_args():
     with pytest.raises(ValueError):
         srb.FieldObjective(fd, [0], [1.0, 2.0], 1.0)
     with pytest.raises(NotImplementedError):
-        srb.FieldObjective(fd, [0] * 129, np.ones(129), 1.0).evaluate(
-            torch.zeros((129, 2, 64), dtype=torch.float64, device=fd.data.device))
+        srb.FieldObjective(fd, [0] * 161, np.ones(161), 1.0).evaluate(  # > SR_MAX_FRAMES = 160
+            torch.zeros((161, 2, 64), dtype=torch.float64, device=fd.data.device))
 
 
 @pytest.mark.parametrize("dims", [(40, 24), (12, 10, 9)])
