@@ -57,9 +57,10 @@ def bytes_per_vf(d: int, s: int) -> dict:
 # itself must move as designed (the split kernels' intermediate reads / writes included).
 def kernel_bytes_per_vf(d: int, s: int) -> dict:
     b = bytes_per_vf(d, s)
-    alg = {"k_ngf_sfeat2": b["pass1"], "k_sample_vp": b["pass1"], "k_pass2_tma": b["pass2"],
+    alg = {"k_ngf_sfeat2": b["pass1"], "k_ngf_sfeat2f": b["pass1"], "k_sample_vp": b["pass1"], "k_pass2_tma": b["pass2"],
            "k_pass2_mma": b["pass2"], "k_ngf_adj4": b["pass2"], "k_pass1": b["pass1"], "k_pass2": b["pass2"]}
     own = {"k_ngf_sfeat2": (1 + d) * s + (3 * d + 1) * s,  # y, T in; n, 1/rho, grad T out
+           "k_ngf_sfeat2f": (1 + d) * s + (3 * d + 1) * s,
            "k_sample_vp": 2 * (1 + d) * s, "k_pass2_tma": (1 + 2 * d) * s, "k_pass2_mma": (1 + 2 * d) * s,
            "k_gram_tma": s, "k_gram_tcx": d * s, "k_ngf_feat4": (3 + d) * s, "k_ngf_z_tc": (2 * d + 1) * s,
            "k_ngf_z_f16": (2 * d + 1) * s, "k_ngf_adj4": 3 * d * s, "k_pass1": b["pass1"], "k_pass2": b["pass2"],

@@ -734,4 +734,193 @@ __global__ void __launch_bounds__(1024 / (4 / PX) <= 512 ? 512 : 256, 2) k_ngf_s
     }
   }
 }
+// ---- k_ngf_sfeat2f: the same rows -> (n, 1/rho, grad T) walk as k_ngf_sfeat2 for the aligned common case
+// (power-of-two spacings, even n0 and strides / offsets: ngf_sfeat_d2 checks), written for instruction
+// count and latency hiding (k_ngf_sfeat2 issued ~227 instructions per voxel-frame and was issue-bound; a
+// first rewrite with the same CTA-per-row shape issued 90 and was bound by the per-row barrier and the
+// gather latency behind it).  Work unit = one WARP: (frame, segment of rows, chunk of 62 columns).  The
+// warp samples 64 columns (its chunk + one halo column each side, clamped into the image, which is
+// exactly u(-1) := u(0), u(n0) := u(n0 - 1)), lane i the columns s + 2 i and s + 2 i + 1, so the x stencil
+// needs only warp shuffles: no shared memory, no barrier, warps drift freely.  Lane i < 31 stores the
+// aligned pair (its second column, lane i + 1's first column).  The u rows rotate through a 3x unrolled
+// loop instead of register moves; row ends are handled by a per-row factor; the power-of-two stencil
+// factors are applied after the rounding to fp32 (identical bits); 1/rho = rsqrt.approx(|p|^2 + eps^2)
+// (2^-22 relative) instead of the IEEE sqrt + division.  Per row: stencil of row r, finish row r + 2
+// from the corners fetched one row earlier, fetch the corners of row r + 3, load the y of row r + 4.
+static __device__ __forceinline__ float rsqrt_fast(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+struct CornersF {
+  float v00, v10, v01, v11, f0, f1;
+  bool inside;
+};
+template <int PF>
+__device__ __forceinline__ CornersF fetch2f(const float* __restrict__ img, float of0, float of1, float iv0, float iv1,
+                                            float hi0, float hi1, int m0, int m1, int s1, float px, float py) {
+  CornersF c;
+  const float t0 = fmaf(__fsub_rn(px, of0), iv0, -0.5f), t1 = fmaf(__fsub_rn(py, of1), iv1, -0.5f);
+  const float c0 = fminf(fmaxf(t0, 0.f), hi0), c1 = fminf(fmaxf(t1, 0.f), hi1);
+  c.inside = (c0 == t0) && (c1 == t1);
+  const int i0 = min(__float2int_rz(c0), m0), i1 = min(__float2int_rz(c1), m1);  // c >= 0: trunc = floor
+  c.f0 = c0 - (float)i0;
+  c.f1 = c1 - (float)i1;
+  const float* q = img + (i0 + i1 * s1);
+  c.v00 = __ldg(q);
+  c.v10 = __ldg(q + 1);
+  c.v01 = __ldg(q + s1);
+  c.v11 = __ldg(q + s1 + 1);
+  if (PF > 0)  // the image rows the next rows of a smooth field will gather from: into L2 ahead of time
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(q + min(PF, m1 + 1 - i1) * s1));
+  return c;
+}
+__device__ __forceinline__ double finish2f(const CornersF& c, float iv0, float iv1, float& g0, float& g1) {
+  const float d0 = c.v10 - c.v00, d1 = c.v11 - c.v01;
+  const float a0f = fmaf(c.f0, d0, c.v00), a1f = fmaf(c.f0, d1, c.v01);
+  const float gv0 = fmaf(c.f1, d1 - d0, d0), gv1 = a1f - a0f;
+  g0 = c.inside ? gv0 * iv0 : 0.f;
+  g1 = c.inside ? gv1 * iv1 : 0.f;
+  const double a0 = fma((double)c.f0, (double)c.v10 - (double)c.v00, (double)c.v00);
+  const double a1 = fma((double)c.f0, (double)c.v11 - (double)c.v01, (double)c.v01);
+  return c.inside ? fma((double)c.f1, a1 - a0, a0) : 0.0;
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(32, MINB) k_ngf_sfeat2f(
+    const Args a, int seg, int rz0, int rz1, int rs0, int rs1, float* __restrict__ Nf,
+    float* __restrict__ IRho, long long zlo, long long zstride, float* __restrict__ Gv, long long vlo,
+    long long vstride) {
+  constexpr int CW = 62;  // output columns per warp
+  // one warp per CTA (32 CTAs per SM): everything but the column is CTA-uniform (uniform registers)
+  const int k = blockIdx.z;
+  const int n0 = a.g.n[0], n1 = a.g.n[1];
+  const int lane = threadIdx.x;
+  const int ch = blockIdx.x;
+  const int ra = rz0 + blockIdx.y * seg, rb = min(ra + seg, rz1);
+  if (ra >= rb) return;
+  const int xa = ch * CW - 1 + 2 * lane;                    // first sampled column (may be -1 or >= n0)
+  const int xs0 = min(max(xa, 0), n0 - 1), xs1 = min(xa + 1, n0 - 1);  // clamped sampling columns
+  const int xe = xa + 1;                                    // first column of the stored pair (even)
+  const bool st_ok = lane < 31 && xe < n0;
+  // Per-frame bases kept in registers (opaque to the compiler, which otherwise rebuilds every address from
+  // the kernel parameters with 64-bit arithmetic): one IMAD.WIDE per access with a 32-bit index.  The
+  // second components sit one (32-bit, checked by the launcher) stride further.
+  const float* img = reinterpret_cast<const float*>(a.frames) + (long long)a.job->frame_index[k] * a.g.N;
+  const float* y0b = reinterpret_cast<const float*>(a.y) + ((long long)(2 * k) * a.y_stride - a.y_off + xs0);
+  float* g0b = Gv + ((long long)(2 * k) * vstride - vlo + xe);
+  float* n0b = Nf + ((long long)(2 * k) * zstride - zlo + xe);
+  float* irb_ = IRho + ((long long)k * zstride - zlo + xe);
+  asm volatile("" : "+l"(img), "+l"(y0b), "+l"(g0b), "+l"(n0b), "+l"(irb_));
+  const unsigned ys = (unsigned)a.y_stride, vs = (unsigned)vstride, zs = (unsigned)zstride;
+  const unsigned dx1 = (unsigned)(xs1 - xs0);  // 0 on a clamped column, else 1
+  const float of0 = a.g.of[0], of1 = a.g.of[1], iv0 = a.g.invf[0], iv1 = a.g.invf[1];
+  const float hi0 = (float)(n0 - 1), hi1 = (float)(n1 - 1);
+  const int m0 = n0 - 2, m1 = n1 - 2, s1 = a.g.sti[1];
+  const float e = (float)a.eps, e2 = e * e;
+  // stencil factors: central 1/(2 s) inside, one-sided 1/s on the first / last column and row
+  const float fxa = (xa > 0 && xa < n0 - 1) ? 0.5f * iv0 : iv0, fxb = (xa + 1 > 0 && xa + 1 < n0 - 1) ? 0.5f * iv0 : iv0;
+  const int glo = max(ra, rs0), ghi = min(rb, rs1);  // rows whose grad T this segment writes
+  const int rlast = min(rb, n1 - 1);                 // last row this segment samples
+
+  float ya0, ya1, yb0, yb1;  // y of one row at the two sampled columns: (y0, y1)
+  CornersF ca, cb;
+  auto load_y = [&](unsigned q) {  // q = r * n0
+    ya0 = __ldg(y0b + q);
+    ya1 = __ldg(y0b + (q + ys));
+    yb0 = __ldg(y0b + (q + dx1));
+    yb1 = __ldg(y0b + (q + dx1 + ys));
+  };
+  // y streams from DRAM (the T gathers mostly hit L1 / L2): rows PD ahead are pulled into L2 so that the
+  // register prefetch (one row of slack) only has to cover the L2 latency
+  constexpr int PD = 10, PT = 6;
+  auto prefetch_y = [&](unsigned q) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(y0b + q));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(y0b + (q + ys)));
+  };
+  auto fetch = [&]() {
+    ca = fetch2f<PT>(img, of0, of1, iv0, iv1, hi0, hi1, m0, m1, s1, ya0, ya1);
+    cb = fetch2f<0>(img, of0, of1, iv0, iv1, hi0, hi1, m0, m1, s1, yb0, yb1);
+  };
+  auto finish = [&](int r, unsigned q, double (&u)[2]) {
+    float g0a, g1a, g0c, g1c;
+    u[0] = finish2f(ca, iv0, iv1, g0a, g1a);
+    u[1] = finish2f(cb, iv0, iv1, g0c, g1c);
+    if (r >= glo && r < ghi) {  // warp-uniform
+      const float g0n = __shfl_down_sync(0xffffffffu, g0a, 1), g1n = __shfl_down_sync(0xffffffffu, g1a, 1);
+      if (st_ok) {
+        *reinterpret_cast<float2*>(g0b + q) = make_float2(g0c, g0n);
+        *reinterpret_cast<float2*>(g0b + (q + vs)) = make_float2(g1c, g1n);
+      }
+    }
+  };
+  // one row; TAIL = the rows r + 2 .. r + 4 may lie past the last sampled row.  q = r * n0.
+  auto step = [&](auto tailc, int r, unsigned q, double (&um)[2], const double (&uc)[2], const double (&up)[2]) {
+    constexpr bool TAIL = decltype(tailc)::value;
+    const double left = __shfl_up_sync(0xffffffffu, uc[1], 1), right = __shfl_down_sync(0xffffffffu, uc[0], 1);
+    const float fy = (r > 0 && r + 1 < n1) ? 0.5f * iv1 : iv1;
+    double uq0 = up[0], uq1 = up[1];
+    if (TAIL && r + 1 >= n1) uq0 = uc[0], uq1 = uc[1];  // u(n1) := u(n1 - 1)
+    const float gxa = (float)(uc[1] - left) * fxa, gxb = (float)(right - uc[0]) * fxb;
+    const float gya = (float)(uq0 - um[0]) * fy, gyb = (float)(uq1 - um[1]) * fy;
+    const float ira = rsqrt_fast(fmaf(gxa, gxa, fmaf(gya, gya, e2)));
+    const float irb = rsqrt_fast(fmaf(gxb, gxb, fmaf(gyb, gyb, e2)));
+    const float nxa = gxa * ira, nya = gya * ira;
+    const float nxn = __shfl_down_sync(0xffffffffu, nxa, 1), nyn = __shfl_down_sync(0xffffffffu, nya, 1);
+    const float irn = __shfl_down_sync(0xffffffffu, ira, 1);
+    if (st_ok) {
+      *reinterpret_cast<float2*>(n0b + q) = make_float2(gxb * irb, nxn);
+      *reinterpret_cast<float2*>(n0b + (q + zs)) = make_float2(gyb * irb, nyn);
+      *reinterpret_cast<float2*>(irb_ + q) = make_float2(irb, irn);
+    }
+    if (!TAIL || r + 2 <= rlast) finish(r + 2, q + 2 * n0, um);  // um is dead: it becomes the next "up"
+    if (!TAIL || r + 3 <= rlast) fetch();
+    if (!TAIL || r + 4 <= rlast) load_y(q + 4 * n0);
+    if (!TAIL) prefetch_y(q + (unsigned)(min(r + PD, rlast) - r) * n0);
+  };
+
+  double u0[2], u1[2], u2[2];
+  unsigned q = (unsigned)(ra * n0);
+#pragma unroll
+  for (int i = -1; i < PD; ++i)
+    if (ra + i >= 0 && ra + i <= rlast) prefetch_y(q + (unsigned)(i * n0));
+  load_y(q);
+  fetch();
+  finish(ra, q, u1);
+  if (ra > 0) {
+    load_y(q - n0);
+    fetch();
+    finish(ra - 1, q - n0, u0);
+  } else {
+    u0[0] = u1[0], u0[1] = u1[1];  // u(row -1) := u(row 0)
+  }
+  u2[0] = u2[1] = 0.0;
+  if (ra + 1 < n1) {
+    load_y(q + n0);
+    fetch();
+    finish(ra + 1, q + n0, u2);
+  }
+  if (ra + 2 <= rlast) {
+    load_y(q + 2 * n0);
+    fetch();
+  }
+  if (ra + 3 <= rlast) load_y(q + 3 * n0);
+  int r = ra;
+  for (; r + 6 <= rlast; r += 3, q += 3 * n0) {  // rows r .. r + 2 with every look-ahead row present
+    step(std::false_type{}, r, q, u0, u1, u2);
+    step(std::false_type{}, r + 1, q + n0, u1, u2, u0);
+    step(std::false_type{}, r + 2, q + 2 * n0, u2, u0, u1);
+  }
+  while (r < rb) {
+    step(std::true_type{}, r, q, u0, u1, u2);
+    if (++r >= rb) break;
+    q += n0;
+    step(std::true_type{}, r, q, u1, u2, u0);
+    if (++r >= rb) break;
+    q += n0;
+    step(std::true_type{}, r, q, u2, u0, u1);
+    ++r;
+    q += n0;
+  }
+}
 }  // namespace sr
