@@ -10,6 +10,7 @@
 //                                          z = (r - n (n.r)) / rho
 //   k_ngf_adj4                             dD/dy = (D_h^T z) grad T
 #pragma once
+#include <cuda_fp16.h>
 
 namespace sr {
 
@@ -515,6 +516,255 @@ __global__ void __launch_bounds__(TGX<KP>::NT, 1) k_gram_tcx(const Args a, const
   }
 }
 
+
+// ------------------------------------------------------------------------------------------
+// k_gram_h (K in 65..112): the raw Gram of k_gram_tcx<128> on kind::f16 operands.  The tf32 kernel is bound
+// by shared-memory traffic and by the per-tile hand-offs, not by DRAM (0.84 GB in 0.35 ms at C3): per
+// 32-pixel tile the tensor core reads 44 KB of fp32 operands, the splitters move 43 KB and the fp64 flush
+// 29 KB.  Here a tile is 64 pixels of one component ([KPN frames x 64] fp32 TMA box, 256-byte rows); the
+// splitters write n = hi + lo as two f16 halves (hi = f16(n), lo = f16(n - hi): the pair carries n to 2^-22
+// relative or 3e-8 absolute, the f16 subnormal spacing, as in k_ngf_z_tc) into one [H (KPN rows); L (KPN rows)]
+// SWIZZLE_128B K-major buffer (64 f16 = one 128-byte row); one M128 N(2 KPN) K16 MMA per 16 pixels gives
+// [H H^T | H L^T] in fp32 TMEM; the flush adds 0.5 HH + HL in fp64 every R tiles, G = A + A^T at the end.  Half the operand bytes and a quarter of
+// the MMA instructions per pixel, half the hand-offs.  max |n| per frame as before (degenerate rule).
+__host__ __device__ constexpr uint32_t umma_idesc_h16(int M, int N) {  // kind::f16, f16 A/B, fp32 D, K-major
+  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+static __device__ __forceinline__ void umma_h16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+struct TGH {
+  // 16 splitter warps, 1 MMA issuer warp, 4 flusher warps (one per TMEM lane quarter), 1 TMA producer warp
+  static constexpr int KP = 128, NSP = 512, NT = NSP + 32 + 128 + 32, TP = 64;
+  static constexpr int NB = 2, NA = 2, R = 32, TS = 256, MAXST = 8;  // R tiles of 64 pixels per TMEM slot
+};
+struct GhLayout {
+  int rows, sbytes, obytes, nst;
+};
+inline GhLayout tgh_layout(int K, size_t smem_cap) {
+  GhLayout L{};
+  L.rows = (K + 15) / 16 * 16;
+  L.sbytes = L.rows * TGH::TP * 4;
+  L.obytes = 2 * L.rows * 128;
+  const size_t fixed = 1024 + (size_t)TGH::NB * L.obytes + 512;
+  const int nst = smem_cap > fixed ? (int)((smem_cap - fixed) / L.sbytes) : 0;
+  L.nst = nst > TGH::MAXST ? TGH::MAXST : nst;
+  return L;
+}
+inline size_t tgh_smem(const GhLayout& L) {
+  return 1024 + (size_t)L.nst * L.sbytes + (size_t)TGH::NB * L.obytes + 512;
+}
+
+// The fp64 accumulators live in the CTA's own partial block in global memory (L2-resident: 131 KB per CTA),
+// transposed (entry (row m, column c) at c * KP + m, so the lane-per-row flush is coalesced); each entry is
+// only ever touched by one thread.  The shared memory they took in k_gram_tcx buys TMA stages instead (6 of
+// 28 KB at K = 100: with 2, the bytes in flight per SM bounded the kernel at 2.9 TB/s).
+template <int DUMMY>
+__global__ void __launch_bounds__(TGH::NT, 1) k_gram_h(const Args a, const __grid_constant__ CUtensorMap xmap,
+                                                       int ntx, int ncomp, const GhLayout lay) {
+  using C = TGH;
+  constexpr int TP = C::TP, NB = C::NB, NA = C::NA, KP = C::KP;
+  const int NST = lay.nst;
+  extern __shared__ __align__(1024) unsigned char smem_gh[];
+  unsigned char* base = smem_gh + ((1024 - (smem_u32(smem_gh) & 1023)) & 1023);
+  unsigned char* Vb = base;                                                      // [NB][2 rows][128 B] SW128
+  float* stage = reinterpret_cast<float*>(base + (size_t)NB * lay.obytes);       // [NST][rows][TP] fp32
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + (size_t)NB * lay.obytes + (size_t)NST * lay.sbytes);
+  uint64_t* st_full = bars;
+  uint64_t* st_free = st_full + C::MAXST;
+  uint64_t* vb_full = st_free + C::MAXST;
+  uint64_t* vb_free = vb_full + NB;
+  uint64_t* acc_full = vb_free + NB;
+  uint64_t* acc_free = acc_full + NA;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_free + NA);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int K = a.K, KPN = lay.rows;
+  const long long ntiles = (long long)ntx * ncomp;
+  const long long nloc = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  // tile n of this CTA = global tile blockIdx.x + n gridDim.x = (column tile tx, component ty), advanced
+  // incrementally (no 64-bit division on the single-thread paths)
+  int ptx = (int)(blockIdx.x % (unsigned)ntx), pty = (int)(blockIdx.x / (unsigned)ntx);
+  const int dtx = (int)(gridDim.x % (unsigned)ntx), dty = (int)(gridDim.x / (unsigned)ntx);
+  auto load_next = [&](int st) {
+    mbar_arrive_expect_tx(&st_full[st], (uint32_t)lay.sbytes);
+    tma_load_3d(stage + (size_t)st * KPN * TP, &xmap, ptx * TP, pty, 0, &st_full[st]);
+    ptx += dtx;
+    pty += dty;
+    if (ptx >= ntx) ptx -= ntx, ++pty;
+  };
+  if (tid == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&st_full[s], 1);
+      mbar_init(&st_free[s], C::NSP / 32);  // one arrival per splitter warp
+    }
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(&vb_full[b], C::NSP / 32);
+      mbar_init(&vb_free[b], 1);
+    }
+    for (int s = 0; s < NA; ++s) {
+      mbar_init(&acc_full[s], 1);
+      mbar_init(&acc_free[s], 128);
+    }
+    fence_mbar_init();
+    tma_prefetch_desc(&xmap);
+  }
+  double* out = a.part + (size_t)blockIdx.x * (KP * KP + 3 * KP);
+  for (int e = tid; e < KP * KP; e += C::NT) __stcg(out + e, 0.0);
+  if (warp == C::NSP / 32) tmem_alloc(tmem_slot, C::TS * NA);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (tid < C::NSP) {
+    // ======================= splitters: a warp takes two stage rows (2 x 256 B) per step, lane = (row of the
+    // pair, 16-byte chunk of 4 columns): conflict-free 128-bit reads; 4 steps cover rows 2 (warp + 16 it) + hl.
+    // The 4 f16 hi (and lo) of a lane are half a 16-byte operand chunk: 64-bit stores, a half-warp fills one
+    // swizzled 128-byte operand row.
+    const int hl = lane >> 4, cl = lane & 15;
+    const int r0 = 2 * warp + hl;  // rows r0 + 32 it
+    const uint32_t soff = (uint32_t)(r0 * TP + 4 * cl) * 4;                      // stage bytes, + 32 TP 4 per step
+    const uint32_t ooff = (uint32_t)((r0 >> 3) * 1024 + (r0 & 7) * 128 + ((((cl >> 1) ^ r0) & 7) << 4) + (cl & 1) * 8);
+    const uint32_t loff = ooff + (uint32_t)KPN * 128;                            // L rows: KPN % 8 == 0
+    float fm[4] = {0.f, 0.f, 0.f, 0.f};
+    int st = 0;
+    uint32_t stph = 0;
+    for (long long n = 0; n < nloc; ++n) {
+      const int b = (int)(n & (NB - 1));
+      mbar_wait(&st_full[st], stph);
+      const unsigned char* src = reinterpret_cast<const unsigned char*>(stage) + (size_t)st * lay.sbytes + soff;
+      uint2 hw[4], lw[4];
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {
+        float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (r0 + 32 * it < KPN) q = *reinterpret_cast<const float4*>(src + it * (32 * TP * 4));
+        fm[it] = fmaxf(fm[it], fmaxf(fmaxf(fabsf(q.x), fabsf(q.y)), fmaxf(fabsf(q.z), fabsf(q.w))));
+        const __half2 h0 = __floats2half2_rn(q.x, q.y), h1 = __floats2half2_rn(q.z, q.w);
+        const float2 f0 = __half22float2(h0), f1 = __half22float2(h1);
+        const __half2 l0 = __floats2half2_rn(q.x - f0.x, q.y - f0.y), l1 = __floats2half2_rn(q.z - f1.x, q.w - f1.y);
+        hw[it] = make_uint2(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1));
+        lw[it] = make_uint2(*reinterpret_cast<const uint32_t*>(&l0), *reinterpret_cast<const uint32_t*>(&l1));
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&st_free[st]);  // the stage is in registers: the producer may refill it
+      if (n >= NB) mbar_wait(&vb_free[b], (uint32_t)(((n >> 1) - 1) & 1));
+      unsigned char* ob = Vb + (size_t)b * lay.obytes;
+#pragma unroll
+      for (int it = 0; it < 4; ++it)
+        if (r0 + 32 * it < KPN) {
+          *reinterpret_cast<uint2*>(ob + ooff + it * 4096) = hw[it];
+          *reinterpret_cast<uint2*>(ob + loff + it * 4096) = lw[it];
+        }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&vb_full[b]);
+      if (++st == NST) st = 0, stph ^= 1;
+    }
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      float v = fm[it];
+#pragma unroll
+      for (int o = 1; o < 16; o <<= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+      const int r = r0 + 32 * it;
+      if (cl == 0) {
+        out[KP * KP + r] = 0.0;  // s: unused by NGF
+        out[KP * KP + KP + r] = r < K ? (double)v : 0.0;
+        out[KP * KP + 2 * KP + r] = r < K ? (double)v : 0.0;
+      }
+    }
+  } else if (warp == C::NSP / 32) {
+    // ======================= issuer
+    if (lane == 0) {
+      const uint32_t idesc = umma_idesc_h16(128, 2 * KPN);
+      for (long long n = 0; n < nloc; ++n) {
+        const long long grp = n / C::R;
+        const bool first = n % C::R == 0, last = n % C::R == C::R - 1 || n == nloc - 1;
+        const int b = (int)(n & (NB - 1)), s = (int)(grp % NA);
+        mbar_wait(&vb_full[b], (uint32_t)((n >> 1) & 1));
+        if (first && grp >= NA) mbar_wait(&acc_free[s], (uint32_t)((grp / NA - 1) & 1));
+        tc_fence_after();
+        const uint32_t o0 = smem_u32(Vb + (size_t)b * lay.obytes);
+        const uint32_t acc = tmem + (uint32_t)(s * C::TS);
+#pragma unroll
+        for (int k16 = 0; k16 < TP / 16; ++k16) {
+          const uint64_t dh = umma_sdesc_sw128(o0 + (uint32_t)(k16 * 32));
+          umma_h16(acc, dh, dh, idesc, (k16 > 0 || !first) ? 1u : 0u);  // A = H (128 rows), B = [H; L]
+        }
+        umma_commit(&vb_free[b]);
+        if (last) umma_commit(&acc_full[s]);
+      }
+    }
+    __syncwarp();
+  } else if (warp == C::NT / 32 - 1) {
+    // ======================= TMA producer: stage of tile n is refilled (tile n + NST) once the splitters have
+    // it in registers (st_free)
+    if (lane == 0) {
+      for (long long n = 0; n < nloc && n < NST; ++n) load_next((int)n);
+      int st = 0;
+      uint32_t ph = 0;
+      for (long long n = 0; n + NST < nloc; ++n) {
+        mbar_wait(&st_free[st], ph);
+        load_next(st);
+        if (++st == NST) st = 0, ph ^= 1;
+      }
+    }
+    __syncwarp();
+  } else {
+    // ======================= flushers: TMEM lane quarter q = warp % 4, row m = 32 q + lane; entry (m, c) of
+    // A = 0.5 HH + HL accumulates at out[c * KP + m]
+    const int q = warp & 3, m = 32 * q + lane;
+    const bool mok = m < KPN;  // TMEM lanes past KPN carry garbage rows (not accumulated)
+    double* acol = out + (mok ? m : 0);
+    const long long ngrp = (nloc + C::R - 1) / C::R;
+    for (long long n = 0; n < ngrp; ++n) {
+      const int s = (int)(n % NA);
+      mbar_wait(&acc_full[s], (uint32_t)((n / NA) & 1));
+      tc_fence_after();
+      const uint32_t ts = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(s * C::TS);
+#pragma unroll 1
+      for (int c0 = 0; c0 < KPN; c0 += 16) {
+        float hh[16], hl[16];
+        double old[16];
+        if (mok) {
+#pragma unroll
+          for (int cc = 0; cc < 16; ++cc) old[cc] = __ldcg(acol + (size_t)(c0 + cc) * KP);
+        }
+        tmem_ld16(ts + (uint32_t)c0, hh);
+        tmem_ld16(ts + (uint32_t)(KPN + c0), hl);
+        if (mok) {
+#pragma unroll
+          for (int cc = 0; cc < 16; ++cc)
+            __stcg(acol + (size_t)(c0 + cc) * KP, old[cc] + (0.5 * (double)hh[cc] + (double)hl[cc]));
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&acc_free[s]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (tid >= C::NSP + 32 && tid < C::NSP + 32 + 128) {
+    // G = A + A^T in place (out holds A^T; the pair (i, j), (j, i) belongs to one thread)
+    const double us = 1.0;
+    for (int e = tid - (C::NSP + 32); e < KP * KP; e += 128) {
+      const int i = e / KP, j = e % KP;
+      if (j < i) continue;
+      const double aij = __ldcg(out + (size_t)j * KP + i), aji = __ldcg(out + (size_t)i * KP + j);
+      const double g = (i < KPN && j < KPN) ? (aij + aji) * us : 0.0;
+      __stcg(out + (size_t)i * KP + j, g);
+      __stcg(out + (size_t)j * KP + i, g);
+    }
+  } else if (warp == C::NSP / 32) {
+    tc_fence_after();
+    tmem_dealloc(tmem, C::TS * NA);
+  }
+}
 
 // ------------------------------------------------------------------------------------------
 // 2-D sampling fused with the NGF feature (replaces k_sample_vp<LO> + k_ngf_feat4 and the u round trip):

@@ -196,7 +196,7 @@ inline cudaError_t ngf_sfeat_d2(const Launch& L, const Args& a, const NgfBufs& B
     // one warp per (chunk of 62 columns, segment of rows, frame): segments as long as >= 4 waves of 32 warps
     // per SM allow (every segment re-samples 2 halo rows and pays an unpipelined prologue)
     const int nchunk = (n0 + 61) / 62;
-    int segf = 64;
+    int segf = 32;
     if (const char* sv = getenv("SEQREG_B200_SFSEG")) segf = atoi(sv) > 0 ? atoi(sv) : segf;
     while (segf > 8 && (long long)((rz1 - rz0 + segf - 1) / segf) * nchunk * a.K < 4LL * 32 * L.sms) segf /= 2;
     const int nseg = (rz1 - rz0 + segf - 1) / segf;
@@ -257,6 +257,32 @@ cudaError_t run_ngf_pass1_kp(const Launch& L, const Args& a, const NgfBufs& B, d
     e = cudaGetLastError();
   }
   if (e != cudaSuccess) return e;
+  if (KP == 128 && !(getenv("SEQREG_B200_GRAMH") && getenv("SEQREG_B200_GRAMH")[0] == '0')) {
+    // K in 65..112: k_gram_h (f16 hi / lo operands, 64-pixel tiles) when its buffers fit the shared memory
+    const GhLayout gl = tgh_layout(a.K, (size_t)smem_cap);
+    const size_t hsm = tgh_smem(gl);
+    CUtensorMap hmap;
+    memset(&hmap, 0, sizeof hmap);
+    cuuint32_t hbox[3] = {(cuuint32_t)TGH::TP, 1, (cuuint32_t)gl.rows};
+    if (gl.nst >= 2 && hsm <= (size_t)smem_cap && 2 * gl.rows <= 256 &&
+        fn(&hmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, B.Nf + (a.pix_lo - B.zlo), gdim, gstr, hbox, es,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
+      e = cudaFuncSetAttribute(k_gram_h<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
+      if (e != cudaSuccess) return e;
+      const int ntxh = (int)((npix + TGH::TP - 1) / TGH::TP);
+      const long long nth = (long long)ntxh * D;
+      int hgrid = L.grid_override > 0 ? L.grid_override : L.sms;
+      if (hgrid > nth) hgrid = (int)nth;
+      const size_t hstride = (size_t)KP * KP + 3 * KP;
+      if ((size_t)hgrid * hstride > part_cap) hgrid = (int)(part_cap / hstride);
+      Args b = a;
+      b.part = part;
+      k_gram_h<0><<<hgrid, TGH::NT, hsm, L.stream>>>(b, hmap, ntxh, D, gl);
+      *nblk = hgrid;
+      return cudaGetLastError();
+    }
+  }
   const size_t smem = tgx_smem<KP>(lay);
   e = cudaFuncSetAttribute(k_gram_tcx<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
