@@ -749,18 +749,34 @@ __global__ void __launch_bounds__(TGH::NT, 1) k_gram_h(const Args a, const __gri
   }
   tc_fence_before();
   __syncthreads();
-  if (tid >= C::NSP + 32 && tid < C::NSP + 32 + 128) {
-    // G = A + A^T in place (out holds A^T; the pair (i, j), (j, i) belongs to one thread)
-    const double us = 1.0;
-    for (int e = tid - (C::NSP + 32); e < KP * KP; e += 128) {
-      const int i = e / KP, j = e % KP;
-      if (j < i) continue;
-      const double aij = __ldcg(out + (size_t)j * KP + i), aji = __ldcg(out + (size_t)i * KP + j);
-      const double g = (i < KPN && j < KPN) ? (aij + aji) * us : 0.0;
-      __stcg(out + (size_t)i * KP + j, g);
-      __stcg(out + (size_t)j * KP + i, g);
+  {
+    // G = A + A^T in place (out holds A^T; the pair (i, j), (j, i) belongs to one thread), every thread of
+    // the CTA, 4 pairs per batch so that the L2 round trips overlap
+    for (int e0 = tid; e0 < KP * KP; e0 += 4 * C::NT) {
+      double x[4], y[4];
+      bool ok[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + u * C::NT, i = e / KP, j = e % KP;
+        ok[u] = e < KP * KP && j >= i;
+        x[u] = y[u] = 0.0;
+        if (ok[u]) {
+          x[u] = __ldcg(out + (size_t)j * KP + i);
+          y[u] = __ldcg(out + (size_t)i * KP + j);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + u * C::NT, i = e / KP, j = e % KP;
+        if (ok[u]) {
+          const double g = (i < KPN && j < KPN) ? x[u] + y[u] : 0.0;
+          __stcg(out + (size_t)i * KP + j, g);
+          __stcg(out + (size_t)j * KP + i, g);
+        }
+      }
     }
-  } else if (warp == C::NSP / 32) {
+  }
+  if (warp == C::NSP / 32) {
     tc_fence_after();
     tmem_dealloc(tmem, C::TS * NA);
   }
