@@ -62,7 +62,7 @@ def kernel_bytes_per_vf(d: int, s: int) -> dict:
     own = {"k_ngf_sfeat2": (1 + d) * s + (3 * d + 1) * s,  # y, T in; n, 1/rho, grad T out
            "k_ngf_sfeat2f": (1 + d) * s + (3 * d + 1) * s,
            "k_sample_vp": 2 * (1 + d) * s, "k_pass2_tma": (1 + 2 * d) * s, "k_pass2_mma": (1 + 2 * d) * s,
-           "k_gram_tma": s, "k_gram_tcx": d * s, "k_gram_h": d * s, "k_ngf_feat4": (3 + d) * s, "k_ngf_z_tc": (2 * d + 1) * s,
+           "k_gram_tma": s, "k_gram_h": d * s, "k_ngf_feat4": (3 + d) * s, "k_ngf_z_tc": (2 * d + 1) * s,
            "k_ngf_z_f16": (2 * d + 1) * s, "k_ngf_adj4": 3 * d * s, "k_pass1": b["pass1"], "k_pass2": b["pass2"],
            "k_reduce_finalize": 0}
     return {"algorithmic": alg, "own": own}

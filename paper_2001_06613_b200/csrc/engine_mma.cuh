@@ -480,7 +480,7 @@ __global__ void __launch_bounds__(GTM::NT * SUP, SUP == 1 ? 2 : 1) k_gram_tma(co
       mx = fmax(mx, rs[(w2 * 32 + k) * 3 + 1]);
       mn = fmin(mn, rs[(w2 * 32 + k) * 3 + 2]);
     }
-    if (NGF) {  // k_gram_tcx's layout: s unused, both extremum slots = max |n| (0 when no pixel)
+    if (NGF) {  // k_gram_h's layout: s unused, both extremum slots = max |n| (0 when no pixel)
       const double am = k < K && mx >= mn ? fmax(mx, -mn) : 0.0;
       out[KP * KP + k] = 0.0;
       out[KP * KP + KP + k] = am;

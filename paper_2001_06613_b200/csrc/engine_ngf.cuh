@@ -1,11 +1,13 @@
 // engine_ngf.cuh — split NGF path (fp32, displacement fields, K <= 128): no neighbour re-sampling,
 // tensor-core Gram, streaming pass 2.  DESIGN.md §4.
 //
-//   k_sample_vp<LO> (engine_tc.cuh)        u = T_k(y_k) (fp64 arithmetic, kept as an fp32 pair) and
-//                                          grad T_k over the slab +- 2 rows
-//   k_ngf_feat4                            n = grad_h u / rho, 1/rho, rho = sqrt(|grad_h u|^2 + eps^2)
-//                                          (the stencil of ngf_at, engine.cuh) over the slab +- 1 row
-//   k_gram_tcx<64|128>                     raw Gram  sum_(p, c) n_i n_j  over the slab on tcgen05 (3xTF32)
+//   k_ngf_sfeat2f (2-D)                    sampling fused with the feature: u = T_k(y_k) (fp64 value),
+//                                          n = grad_h u / rho, 1/rho, grad T_k; one warp per (frame, row
+//                                          segment, 62-column chunk); k_ngf_sfeat2 = its generic fallback
+//   k_sample_vp<LO> (engine_tc.cuh)        3-D: u (fp64 arithmetic, kept as an fp32 pair) and grad T_k over
+//   + k_ngf_feat4                          the slab +- 2 rows, then n, 1/rho (the stencil of ngf_at)
+//   k_gram_h<64|128>                       raw Gram  sum_(p, c) n_i n_j  over the slab on tcgen05 (kind::f16,
+//                                          hi / lo split), K > 32; k_gram_tma<NGF> (mma.sync) for K <= 32
 //   k_ngf_z_tc (engine_ngf_tc.cuh)         r = M'^T n (per pixel and component) on tcgen05,
 //                                          z = (r - n (n.r)) / rho
 //   k_ngf_adj4                             dD/dy = (D_h^T z) grad T
@@ -267,261 +269,11 @@ __global__ void __launch_bounds__(256) k_ngf_adj4(const Args a, const float* __r
 }
 
 // ------------------------------------------------------------------------------------------
-// Raw NGF Gram G_ij = sum over the slab's pixels and components of n_i n_j, for up to 128 frames.
-// Tiles of 32 columns of one component ([128 frames x 32] TMA box of a 3-D map over
-// Nf [K][D][zstride], zero fill past K and past the slab); 16 splitter warps turn a tile into
-// hi/lo tf32 halves (SWIZZLE_128B, K-major) and keep max |n| per frame; one lane issues per K8
-// step three M128 N128 K8 MMAs (hi.hi^T, lo.hi^T, hi.lo^T) into one TMEM slot (R tiles per slot,
-// ring of NA slots); 4 flusher warps add the slot into fp64 accumulators in shared memory, whose
-// column index is XOR-swizzled by the row (conflict-free for a lane-per-row flush).
-// KP = 128: hi (128 rows) and lo operands; per K8 step three M128 N128 MMAs (hi.hi^T + lo.hi^T +
-// hi.lo^T) give G directly.  KP = 64: one 128-row operand [hi (64 rows); lo (64 rows)] and one
-// M128 N64 MMA per K8 step (B = the hi rows) give HH (rows 0-63) and LH (rows 64-127);
-// G = HH + LH + LH^T at the end.
-template <int KP_>
-struct TGX {
-  static constexpr int KP = KP_;
-  static constexpr int NSP = 512, NT = NSP + 32 + 128;
-  static constexpr int TP = KP == 64 ? 64 : 32;  // columns per tile (shared-memory bound at KP = 128)
-  // R tiles accumulate in a TMEM slot (fp32, 512 columns) between fp64 flushes: the flush of a
-  // 128 x N slot, not the MMAs, bounds this kernel (R = 4 -> 16 at KP = 128: 0.71 -> 0.45 ms at C3)
-  static constexpr int NST = 2, NB = 2, NA = 2, R = KP == 64 ? 8 : 16;
-  // KP = 128: one MMA per K8 step, A = H (rows 0..127 of the [H (KPN rows); L (KPN rows)] buffer), B = the
-  // whole buffer (N = 2 KPN, KPN = K rounded up to 16): D = [H H^T | H L^T]; the flush accumulates
-  // 0.5 HH + HL in fp64 and G = A + A^T at the end (= HH + HL + LH).  (0.58x the tensor work of the
-  // three N = 128 MMAs hi.hi + lo.hi + hi.lo.)
-  static constexpr int N = KP == 128 ? 256 : KP;  // TMEM columns per slot (MMA N = 2 KPN <= 256 at KP = 128)
-  static constexpr int SBYTES = KP * TP * 4;     // fp32 stage [KP][32]
-  static constexpr int OBYTES = (KP == 128 ? 256 : 128) * TP * 4;  // [H; L] rows x TP columns (KP = 64: [hi; lo])
-  static constexpr int NOPS = 1;
-  static constexpr uint32_t IDESC = umma_idesc_tf32(128, KP);  // KP = 64 (KP = 128 uses the runtime N = 2 KPN)
-  static constexpr int ACC_ROWS = 128, ACC_COLS = KP == 128 ? 128 : N;
-};
-
-// Runtime shared-memory layout of k_gram_tcx: at KP = 128 the stage (= TMA box) and operand rows follow
-// KPN = K rounded up to 16 instead of 128, and the bytes saved buy TMA stages (K = 100: 4 instead of 2 —
-// a 16 KB tile takes longer to arrive than its four K8 steps take on the tensor core).
-struct GxLayout {
-  int rows;      // stage rows (frames per TMA box)
-  int nst;       // TMA stages
-  int sbytes;    // bytes per stage
-  int obytes;    // bytes per operand buffer
-  int acc_rows;  // fp64 accumulator rows (row width ACC_COLS)
-};
-constexpr int kGxMaxStages = 6;
-
-template <int KP>
-inline GxLayout tgx_layout(int K, size_t smem_cap) {
-  using C = TGX<KP>;
-  GxLayout L{};
-  const int kpn = (K + 15) / 16 * 16;
-  L.rows = KP == 128 ? kpn : KP;
-  L.sbytes = L.rows * C::TP * 4;
-  L.obytes = KP == 128 ? 2 * kpn * 128 : C::OBYTES;
-  L.acc_rows = KP == 128 ? kpn : C::ACC_ROWS;
-  const size_t fixed = 1024 + (size_t)C::NB * L.obytes + (size_t)L.acc_rows * C::ACC_COLS * 8 + 512;
-  int nst = smem_cap > fixed ? (int)((smem_cap - fixed) / L.sbytes) : 0;
-  L.nst = nst < 2 ? 2 : nst > kGxMaxStages ? kGxMaxStages : nst;
-  return L;
-}
-template <int KP>
-inline size_t tgx_smem(const GxLayout& L) {
-  using C = TGX<KP>;
-  return 1024 + (size_t)L.nst * L.sbytes + (size_t)C::NB * L.obytes + (size_t)L.acc_rows * C::ACC_COLS * 8 + 512;
-}
-
-template <int KP>
-__global__ void __launch_bounds__(TGX<KP>::NT, 1) k_gram_tcx(const Args a, const __grid_constant__ CUtensorMap xmap,
-                                                            int ntx, int ncomp, const GxLayout lay) {
-  using C = TGX<KP>;
-  constexpr int TP = C::TP, NB = C::NB, NA = C::NA, NC = C::ACC_COLS;
-  const int NST = lay.nst;
-  extern __shared__ __align__(1024) unsigned char smem_gx[];
-  unsigned char* base = smem_gx + ((1024 - (smem_u32(smem_gx) & 1023)) & 1023);
-  float* stage = reinterpret_cast<float*>(base);                                       // [NST][rows][TP]
-  unsigned char* Vb = base + (size_t)NST * lay.sbytes;                                 // [NB][operand]
-  double* accs = reinterpret_cast<double*>(Vb + (size_t)NB * lay.obytes);              // [acc_rows][NC] swizzled
-  uint64_t* bars = reinterpret_cast<uint64_t*>(accs + (size_t)lay.acc_rows * NC);
-  uint64_t* st_full = bars;
-  uint64_t* vb_full = st_full + kGxMaxStages;
-  uint64_t* vb_free = vb_full + NB;
-  uint64_t* acc_full = vb_free + NB;
-  uint64_t* acc_free = acc_full + NA;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_free + NA);
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int K = a.K;
-  const long long ntiles = (long long)ntx * ncomp;
-  const long long nloc = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  auto load_tile = [&](long long n, int st) {
-    const long long t = blockIdx.x + n * gridDim.x;
-    mbar_arrive_expect_tx(&st_full[st], (uint32_t)lay.sbytes);
-    tma_load_3d(stage + (size_t)st * lay.rows * TP, &xmap, (int)(t % ntx) * TP, (int)(t / ntx), 0, &st_full[st]);
-  };
-  if (tid == 0) {
-    for (int s = 0; s < NST; ++s) mbar_init(&st_full[s], 1);
-    for (int b = 0; b < NB; ++b) {
-      mbar_init(&vb_full[b], C::NSP);
-      mbar_init(&vb_free[b], 1);
-    }
-    for (int s = 0; s < NA; ++s) {
-      mbar_init(&acc_full[s], 1);
-      mbar_init(&acc_free[s], 128);
-    }
-    fence_mbar_init();
-    tma_prefetch_desc(&xmap);
-  }
-  for (int e = tid; e < lay.acc_rows * NC; e += C::NT) accs[e] = 0.0;
-  const int KPN = KP == 128 ? (K + 15) / 16 * 16 : KP;  // rows of H (and of L) in the KP = 128 buffer
-  constexpr int TS = C::N;                              // TMEM columns per slot
-  if (warp == C::NSP / 32) tmem_alloc(tmem_slot, TS * NA);
-  fence_proxy_async_smem();
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  double* out = a.part + (size_t)blockIdx.x * (KP * KP + 3 * KP);
-
-  if (tid < C::NSP) {
-    // ======================= splitters: KP = 128: row r = tid / 4, 8 columns; KP = 64: row tid / 8, 4 columns
-    constexpr int TPR = C::NSP / KP;  // threads per row
-    constexpr int CPT = TP / TPR;     // columns per thread (8 or 4)
-    const int r = tid / TPR, part = tid % TPR;
-    float fmx = 0.f;
-    for (long long n = 0; n < nloc; ++n) {
-      const int b = (int)(n % NB), st = (int)(n % NST);
-      mbar_wait(&st_full[st], (uint32_t)((n / NST) & 1));
-      const bool rok = r < lay.rows;  // KP = 128: rows past KPN are not staged
-      const float* src = stage + (size_t)st * lay.rows * TP + (size_t)r * TP + part * CPT;
-      float4 qq[CPT / 4];
-#pragma unroll
-      for (int h = 0; h < CPT / 4; ++h)
-        qq[h] = rok ? *reinterpret_cast<const float4*>(src + 4 * h) : make_float4(0.f, 0.f, 0.f, 0.f);
-      if (n >= NB) mbar_wait(&vb_free[b], (uint32_t)((n / NB - 1) & 1));
-      unsigned char* ob = Vb + (size_t)b * lay.obytes;
-#pragma unroll
-      for (int h = 0; h < CPT / 4; ++h) {
-        const float qv[4] = {qq[h].x, qq[h].y, qq[h].z, qq[h].w};
-        float hi[4], lo[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          fmx = fmaxf(fmx, fabsf(qv[u]));
-          hi[u] = to_tf32(qv[u]);
-          lo[u] = qv[u] - hi[u];
-        }
-        const int col = part * CPT + 4 * h;
-        const int atom = col >> 5, g = (col & 31) >> 2;  // column atom (TP = 32 at KP = 128), 16-byte chunk
-        const int rh = r, rl = KP == 128 ? KPN + r : 64 + r;
-        if (KP != 128 || r < KPN) {
-          unsigned char* hb = ob + atom * (128 * 128);
-          *reinterpret_cast<float4*>(hb + (rh >> 3) * 1024 + (rh & 7) * 128 + (((g ^ (rh & 7)) & 7) << 4)) =
-              make_float4(hi[0], hi[1], hi[2], hi[3]);
-          *reinterpret_cast<float4*>(hb + (rl >> 3) * 1024 + (rl & 7) * 128 + (((g ^ (rl & 7)) & 7) << 4)) =
-              make_float4(lo[0], lo[1], lo[2], lo[3]);
-        }
-      }
-      fence_proxy_async_smem();
-      mbar_arrive(&vb_full[b]);  // also releases stage st
-    }
-#pragma unroll
-    for (int o = 1; o < TPR; o <<= 1) fmx = fmaxf(fmx, __shfl_xor_sync(0xffffffffu, fmx, o));
-    if (part == 0) {
-      out[KP * KP + r] = 0.0;  // s: unused by NGF
-      out[KP * KP + KP + r] = r < K ? (double)fmx : 0.0;
-      out[KP * KP + 2 * KP + r] = r < K ? (double)fmx : 0.0;
-    }
-  } else if (warp == C::NSP / 32) {
-    // ======================= issuer
-    if (lane == 0) {
-      for (long long n = 0; n < nloc && n < NST; ++n) load_tile(n, (int)n);
-      for (long long n = 0; n < nloc; ++n) {
-        const long long grp = n / C::R;
-        const bool first = n % C::R == 0, last = n % C::R == C::R - 1 || n == nloc - 1;
-        const int b = (int)(n % NB), s = (int)(grp % NA), st = (int)(n % NST);
-        mbar_wait(&vb_full[b], (uint32_t)((n / NB) & 1));
-        if (n + NST < nloc) load_tile(n + NST, st);
-        if (first && grp >= NA) mbar_wait(&acc_free[s], (uint32_t)((grp / NA - 1) & 1));
-        tc_fence_after();
-        const uint32_t o0 = smem_u32(Vb + (size_t)b * lay.obytes);
-        const uint32_t acc = tmem + (uint32_t)(s * TS);
-        const uint32_t idesc = KP == 128 ? umma_idesc_tf32(128, 2 * KPN) : C::IDESC;
-#pragma unroll
-        for (int k8 = 0; k8 < TP / 8; ++k8) {
-          const uint32_t acc_in = (k8 > 0 || !first) ? 1u : 0u;
-          const uint32_t koff = (uint32_t)((k8 >> 2) * (128 * 128) + (k8 & 3) * 32);
-          const uint64_t dh = umma_sdesc_sw128(o0 + koff);
-          // KP = 128: A = H (128 rows from the buffer start), B = [H; L] (2 KPN rows); KP = 64: A = [hi; lo]
-          // (128 rows), B = hi (first 64 rows)
-          umma_tf32(acc, dh, dh, idesc, acc_in);
-        }
-        umma_commit(&vb_free[b]);
-        if (last) umma_commit(&acc_full[s]);
-      }
-    }
-    __syncwarp();
-  } else {
-    // ======================= flushers: TMEM lane quarter q = warp % 4, row m = 32 q + lane
-    const int q = warp & 3, m = 32 * q + lane;
-    const bool mok = m < lay.acc_rows;  // KP = 128: TMEM lanes past KPN carry garbage rows (not accumulated)
-    double* arow = accs + (size_t)(mok ? m : 0) * NC;
-    const long long ngrp = (nloc + C::R - 1) / C::R;
-    for (long long n = 0; n < ngrp; ++n) {
-      const int s = (int)(n % NA);
-      mbar_wait(&acc_full[s], (uint32_t)((n / NA) & 1));
-      tc_fence_after();
-      const uint32_t ts = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(s * TS);
-      if (KP == 128) {  // 0.5 HH + HL, 32 (last: 16) columns at a time
-#pragma unroll 1
-        for (int c0 = 0; c0 < KPN; c0 += 32) {
-          if (c0 + 32 <= KPN) {
-            float hh[32], hl[32];
-            tmem_ld32(ts + (uint32_t)c0, hh);
-            tmem_ld32(ts + (uint32_t)(KPN + c0), hl);
-#pragma unroll
-            for (int cc = 0; cc < 32; ++cc)
-              if (mok) arow[(c0 + cc) ^ lane] += 0.5 * (double)hh[cc] + (double)hl[cc];
-          } else {
-            float hh[16], hl[16];
-            tmem_ld16(ts + (uint32_t)c0, hh);
-            tmem_ld16(ts + (uint32_t)(KPN + c0), hl);
-#pragma unroll
-            for (int cc = 0; cc < 16; ++cc)
-              if (mok) arow[(c0 + cc) ^ lane] += 0.5 * (double)hh[cc] + (double)hl[cc];
-          }
-        }
-      } else {
-#pragma unroll 1
-        for (int ch = 0; ch < NC / 32; ++ch) {
-          float v[32];
-          tmem_ld32(ts + (uint32_t)(ch * 32), v);
-#pragma unroll
-          for (int cc = 0; cc < 32; ++cc) arow[(32 * ch + cc) ^ lane] += (double)v[cc];
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(&acc_free[s]);
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (tid >= C::NSP + 32) {
-    auto A = [&](int i, int j) { return accs[(size_t)i * NC + (j ^ (i & 31))]; };
-    for (int e = tid - (C::NSP + 32); e < KP * KP; e += 128) {
-      const int i = e / KP, j = e % KP;
-      out[e] = KP == 128 ? (i < KPN && j < KPN ? A(i, j) + A(j, i) : 0.0) : A(i, j) + A(64 + i, j) + A(64 + j, i);
-    }
-  } else if (warp == C::NSP / 32) {
-    tc_fence_after();
-    tmem_dealloc(tmem, TS * NA);
-  }
-}
-
-
-// ------------------------------------------------------------------------------------------
-// k_gram_h (K in 65..112): the raw Gram of k_gram_tcx<128> on kind::f16 operands.  The tf32 kernel is bound
-// by shared-memory traffic and by the per-tile hand-offs, not by DRAM (0.84 GB in 0.35 ms at C3): per
-// 32-pixel tile the tensor core reads 44 KB of fp32 operands, the splitters move 43 KB and the fp64 flush
-// 29 KB.  Here a tile is 64 pixels of one component ([KPN frames x 64] fp32 TMA box, 256-byte rows); the
+// k_gram_h (K in 33..128): raw NGF Gram G_ij = sum over the slab's pixels and components of n_i n_j on
+// tcgen05 kind::f16 operands with TMEM accumulators.  (Its round-2 predecessor k_gram_tcx — kind::tf32 hi / lo
+// split of 32-pixel tiles, fp64 accumulators in shared memory — was bound by shared-memory traffic and the
+// per-tile hand-offs, not by DRAM: 0.84 GB in 0.35 ms at C3; per 32-pixel tile the tensor core read 44 KB of
+// fp32 operands, the splitters moved 43 KB and the fp64 flush 29 KB.)  Here a tile is 64 pixels of one component ([KPN frames x 64] fp32 TMA box, 256-byte rows); the
 // splitters write n = hi + lo as two f16 halves (hi = f16(n), lo = f16(n - hi): the pair carries n to 2^-22
 // relative or 3e-8 absolute, the f16 subnormal spacing, as in k_ngf_z_tc) into one [H (KPN rows); L (KPN rows)]
 // SWIZZLE_128B K-major buffer (64 f16 = one 128-byte row); one M128 N(2 KPN) K16 MMA per 16 pixels gives
@@ -539,8 +291,8 @@ static __device__ __forceinline__ void umma_h16(uint32_t tmem_d, uint64_t adesc,
 }
 struct TGH {
   // 16 splitter warps, 1 MMA issuer warp, 4 flusher warps (one per TMEM lane quarter), 1 TMA producer warp
-  static constexpr int KP = 128, NSP = 512, NT = NSP + 32 + 128 + 32, TP = 64;
-  static constexpr int NB = 2, NA = 2, R = 32, TS = 256, MAXST = 8;  // R tiles of 64 pixels per TMEM slot
+  static constexpr int NSP = 512, NT = NSP + 32 + 128 + 32, TP = 64;
+  static constexpr int NB = 3, NA = 2, R = 32, TS = 256, MAXST = 8;  // R tiles of 64 pixels per TMEM slot
 };
 struct GhLayout {
   int rows, sbytes, obytes, nst;
@@ -563,11 +315,11 @@ inline size_t tgh_smem(const GhLayout& L) {
 // transposed (entry (row m, column c) at c * KP + m, so the lane-per-row flush is coalesced); each entry is
 // only ever touched by one thread.  The shared memory they took in k_gram_tcx buys TMA stages instead (6 of
 // 28 KB at K = 100: with 2, the bytes in flight per SM bounded the kernel at 2.9 TB/s).
-template <int DUMMY>
+template <int KP>  // KP = 64 or 128: the partial block layout [KP x KP | s | vmax | -vmin] of the K bucket
 __global__ void __launch_bounds__(TGH::NT, 1) k_gram_h(const Args a, const __grid_constant__ CUtensorMap xmap,
                                                        int ntx, int ncomp, const GhLayout lay) {
   using C = TGH;
-  constexpr int TP = C::TP, NB = C::NB, NA = C::NA, KP = C::KP;
+  constexpr int TP = C::TP, NB = C::NB, NA = C::NA;
   const int NST = lay.nst;
   extern __shared__ __align__(1024) unsigned char smem_gh[];
   unsigned char* base = smem_gh + ((1024 - (smem_u32(smem_gh) & 1023)) & 1023);
@@ -636,7 +388,7 @@ __global__ void __launch_bounds__(TGH::NT, 1) k_gram_h(const Args a, const __gri
     int st = 0;
     uint32_t stph = 0;
     for (long long n = 0; n < nloc; ++n) {
-      const int b = (int)(n & (NB - 1));
+      const int b = (int)(n % NB);
       mbar_wait(&st_full[st], stph);
       const unsigned char* src = reinterpret_cast<const unsigned char*>(stage) + (size_t)st * lay.sbytes + soff;
       uint2 hw[4], lw[4];
@@ -653,7 +405,7 @@ __global__ void __launch_bounds__(TGH::NT, 1) k_gram_h(const Args a, const __gri
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&st_free[st]);  // the stage is in registers: the producer may refill it
-      if (n >= NB) mbar_wait(&vb_free[b], (uint32_t)(((n >> 1) - 1) & 1));
+      if (n >= NB) mbar_wait(&vb_free[b], (uint32_t)((n / NB - 1) & 1));
       unsigned char* ob = Vb + (size_t)b * lay.obytes;
 #pragma unroll
       for (int it = 0; it < 4; ++it)
@@ -672,7 +424,7 @@ __global__ void __launch_bounds__(TGH::NT, 1) k_gram_h(const Args a, const __gri
 #pragma unroll
       for (int o = 1; o < 16; o <<= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
       const int r = r0 + 32 * it;
-      if (cl == 0) {
+      if (cl == 0 && r < KP) {
         out[KP * KP + r] = 0.0;  // s: unused by NGF
         out[KP * KP + KP + r] = r < K ? (double)v : 0.0;
         out[KP * KP + 2 * KP + r] = r < K ? (double)v : 0.0;
@@ -685,8 +437,8 @@ __global__ void __launch_bounds__(TGH::NT, 1) k_gram_h(const Args a, const __gri
       for (long long n = 0; n < nloc; ++n) {
         const long long grp = n / C::R;
         const bool first = n % C::R == 0, last = n % C::R == C::R - 1 || n == nloc - 1;
-        const int b = (int)(n & (NB - 1)), s = (int)(grp % NA);
-        mbar_wait(&vb_full[b], (uint32_t)((n >> 1) & 1));
+        const int b = (int)(n % NB), s = (int)(grp % NA);
+        mbar_wait(&vb_full[b], (uint32_t)((n / NB) & 1));
         if (first && grp >= NA) mbar_wait(&acc_free[s], (uint32_t)((grp / NA - 1) & 1));
         tc_fence_after();
         const uint32_t o0 = smem_u32(Vb + (size_t)b * lay.obytes);

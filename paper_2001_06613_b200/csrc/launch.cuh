@@ -222,23 +222,26 @@ inline cudaError_t ngf_sfeat_d2(const Launch& L, const Args& a, const NgfBufs& B
 template <int D, int KP>
 cudaError_t run_ngf_pass1_kp(const Launch& L, const Args& a, const NgfBufs& B, double* part, size_t part_cap,
                              int* nblk) {
-  using C = TGX<KP>;
   const long long npix = a.pix_hi - a.pix_lo;
   if (npix <= 0 || a.K > KP) return cudaErrorNotSupported;
   if (((a.pix_lo - B.zlo) * 4) % 16 || (B.zstride * 4) % 16 || (reinterpret_cast<uintptr_t>(B.Nf) & 15))
     return cudaErrorNotSupported;
   EncodeTiledFn fn = encode_tiled_fn();
   if (!fn) return cudaErrorNotSupported;
-  CUtensorMap xmap;
-  memset(&xmap, 0, sizeof xmap);
-  cuuint64_t gdim[3] = {(cuuint64_t)npix, (cuuint64_t)D, (cuuint64_t)a.K};
-  cuuint64_t gstr[2] = {(cuuint64_t)B.zstride * 4, (cuuint64_t)D * B.zstride * 4};
   int smem_cap = 0;
   cudaDeviceGetAttribute(&smem_cap, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0);
-  const GxLayout lay = tgx_layout<KP>(a.K, (size_t)smem_cap);
-  cuuint32_t box[3] = {(cuuint32_t)C::TP, 1, (cuuint32_t)lay.rows};
+  // k_gram_h: [KPN frames x 64 pixels] fp32 boxes of one component of Nf [K][D][zstride], zero fill past K and
+  // past the slab
+  const GhLayout gl = tgh_layout(a.K, (size_t)smem_cap);
+  const size_t hsm = tgh_smem(gl);
+  CUtensorMap hmap;
+  memset(&hmap, 0, sizeof hmap);
+  cuuint64_t gdim[3] = {(cuuint64_t)npix, (cuuint64_t)D, (cuuint64_t)a.K};
+  cuuint64_t gstr[2] = {(cuuint64_t)B.zstride * 4, (cuuint64_t)D * B.zstride * 4};
+  cuuint32_t hbox[3] = {(cuuint32_t)TGH::TP, 1, (cuuint32_t)gl.rows};
   cuuint32_t es[3] = {1, 1, 1};
-  if (fn(&xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, B.Nf + (a.pix_lo - B.zlo), gdim, gstr, box, es,
+  if (gl.nst < 2 || hsm > (size_t)smem_cap || 2 * gl.rows > 256 ||
+      fn(&hmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, B.Nf + (a.pix_lo - B.zlo), gdim, gstr, hbox, es,
          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorNotSupported;
@@ -257,36 +260,9 @@ cudaError_t run_ngf_pass1_kp(const Launch& L, const Args& a, const NgfBufs& B, d
     e = cudaGetLastError();
   }
   if (e != cudaSuccess) return e;
-  if (KP == 128 && !(getenv("SEQREG_B200_GRAMH") && getenv("SEQREG_B200_GRAMH")[0] == '0')) {
-    // K in 65..112: k_gram_h (f16 hi / lo operands, 64-pixel tiles) when its buffers fit the shared memory
-    const GhLayout gl = tgh_layout(a.K, (size_t)smem_cap);
-    const size_t hsm = tgh_smem(gl);
-    CUtensorMap hmap;
-    memset(&hmap, 0, sizeof hmap);
-    cuuint32_t hbox[3] = {(cuuint32_t)TGH::TP, 1, (cuuint32_t)gl.rows};
-    if (gl.nst >= 2 && hsm <= (size_t)smem_cap && 2 * gl.rows <= 256 &&
-        fn(&hmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, B.Nf + (a.pix_lo - B.zlo), gdim, gstr, hbox, es,
-           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
-      e = cudaFuncSetAttribute(k_gram_h<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
-      if (e != cudaSuccess) return e;
-      const int ntxh = (int)((npix + TGH::TP - 1) / TGH::TP);
-      const long long nth = (long long)ntxh * D;
-      int hgrid = L.grid_override > 0 ? L.grid_override : L.sms;
-      if (hgrid > nth) hgrid = (int)nth;
-      const size_t hstride = (size_t)KP * KP + 3 * KP;
-      if ((size_t)hgrid * hstride > part_cap) hgrid = (int)(part_cap / hstride);
-      Args b = a;
-      b.part = part;
-      k_gram_h<0><<<hgrid, TGH::NT, hsm, L.stream>>>(b, hmap, ntxh, D, gl);
-      *nblk = hgrid;
-      return cudaGetLastError();
-    }
-  }
-  const size_t smem = tgx_smem<KP>(lay);
-  e = cudaFuncSetAttribute(k_gram_tcx<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  e = cudaFuncSetAttribute(k_gram_h<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
   if (e != cudaSuccess) return e;
-  const int ntx = (int)((npix + C::TP - 1) / C::TP);
+  const int ntx = (int)((npix + TGH::TP - 1) / TGH::TP);
   const long long ntiles = (long long)ntx * D;
   int grid = L.grid_override > 0 ? L.grid_override : L.sms;
   if (grid > ntiles) grid = (int)ntiles;
@@ -294,7 +270,7 @@ cudaError_t run_ngf_pass1_kp(const Launch& L, const Args& a, const NgfBufs& B, d
   if ((size_t)grid * stride > part_cap) grid = (int)(part_cap / stride);
   Args b = a;
   b.part = part;
-  k_gram_tcx<KP><<<grid, C::NT, smem, L.stream>>>(b, xmap, ntx, D, lay);
+  k_gram_h<KP><<<grid, TGH::NT, hsm, L.stream>>>(b, hmap, ntx, D, gl);
   *nblk = grid;
   return cudaGetLastError();
 }

@@ -12,7 +12,7 @@ for c in c3 c4 c2; do
 done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"^k_" -c 400 --csv \
   --log-file "$out/launches_c3.csv" python bench.py --steps 2 --warmup 1 --only --no-cpu > "$out/launches_c3.log" 2>&1
-for k in k_ngf_sfeat2 k_gram_tcx k_ngf_z_tc k_ngf_adj4; do
+for k in k_ngf_sfeat2f k_gram_h k_ngf_z_tc k_ngf_adj4; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:"^$k" -c 1 -o "$out/full_c3_$k" \
     python scripts/evalloop.py --config c3 --reps 1 > /dev/null 2>&1
 done

@@ -15,7 +15,7 @@ ROOT = Path(__file__).resolve().parents[1]
 LIB = ROOT / "paper_2001_06613_b200" / "libseqreg_b200.so"
 WATCH = ["UTCHMMA", "UTCQMMA", "UTCBAR", "UTMALDG", "UBLKCP", "LDTM", "STTM", "HMMA", "LDSM", "DFMA", "DADD",
          "F2F", "SHFL", "LDG", "STG", "LDS", "STS", "SYNCS"]
-KEEP = ["k_ngf_sfeat2", "k_gram_tcx", "k_ngf_z_tc", "k_ngf_adj4", "k_reduce_finalize", "k_sample_vp", "k_gram_tma",
+KEEP = ["k_ngf_sfeat2f", "k_gram_h", "k_ngf_z_tc", "k_ngf_adj4", "k_reduce_finalize", "k_sample_vp", "k_gram_tma",
         "k_pass2_tma", "k_pass2_mma", "k_ngf_z_f16", "k_ngf_feat4", "k_pass1_ws", "k_pass1<", "k_pass2<"]
 
 
