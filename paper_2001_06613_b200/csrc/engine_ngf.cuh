@@ -851,7 +851,7 @@ __global__ void __launch_bounds__(32, MINB) k_ngf_sfeat2f(
   };
   // y streams from DRAM (the T gathers mostly hit L1 / L2): rows PD ahead are pulled into L2 so that the
   // register prefetch (one row of slack) only has to cover the L2 latency
-  constexpr int PD = 10, PT = 6;
+  constexpr int PD = 10, PT = 0;
   auto prefetch_y = [&](unsigned q) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(y0b + q));
     asm volatile("prefetch.global.L2 [%0];" ::"l"(y0b + (q + ys)));
