@@ -214,7 +214,7 @@ __global__ void __maxnreg__(96) k_ngf_z_tc(const Args a, const float* __restrict
       const long long t = blockIdx.x + n * gridDim.x;
 #pragma unroll
       for (int m = 0; m < C::MAXU; ++m) {
-        const int u = wq + C::WPQ * m, mt = u / nfg, fg = u % nfg;
+        const int u = wq + C::WPQ * m, mt = u >= nfg ? 1 : 0, fg = u - mt * nfg;  // MT <= 2: no division
         const int p = (int)(t * TP) + mt * PXT + PXW * qb + pxl;
         const bool ok = lane_ok && p < nzp;
         // running pointer over the unit's 8 frames (one 64-bit add per load)
@@ -242,7 +242,7 @@ __global__ void __maxnreg__(96) k_ngf_z_tc(const Args a, const float* __restrict
       const long long t = blockIdx.x + n * gridDim.x;
 #pragma unroll
       for (int m = 0; m < C::MAXU; ++m) {
-        const int u = wq + C::WPQ * m, mt = u / nfg, fg = u % nfg;
+        const int u = wq + C::WPQ * m, mt = u >= nfg ? 1 : 0, fg = u - mt * nfg;  // MT <= 2: no division
         const int p = (int)(t * TP) + mt * PXT + PXW * qb + pxl;
         const bool ok = lane_ok && p < nzp;
         const float* rb = IRho + (ok ? (unsigned)p : 0u);
@@ -259,7 +259,7 @@ __global__ void __maxnreg__(96) k_ngf_z_tc(const Args a, const float* __restrict
       if (n >= NST) mbar_wait_sleep(&a_free[s], (uint32_t)((n / NST - 1) & 1));
 #pragma unroll
       for (int m = 0; m < C::MAXU; ++m) {
-        const int u = wq + C::WPQ * m, mt = u / nfg, fg = u % nfg;
+        const int u = wq + C::WPQ * m, mt = u >= nfg ? 1 : 0, fg = u - mt * nfg;  // MT <= 2: no division
         if (u < nun) {
           unsigned char* Ah = Ab + s * ASTAGE + (size_t)(2 * mt) * AOP;
           unsigned char* Al = Ah + AOP;
@@ -291,7 +291,7 @@ __global__ void __maxnreg__(96) k_ngf_z_tc(const Args a, const float* __restrict
       tc_fence_after();
 #pragma unroll
       for (int m = 0; m < C::MAXU; ++m) {
-        const int u = wq + C::WPQ * m, mt = u / nfg, ch = u % nfg;
+        const int u = wq + C::WPQ * m, mt = u >= nfg ? 1 : 0, ch = u - mt * nfg;
         if (u >= nun) break;
         const int p = (int)(t * TP) + mt * PXT + PXW * qb + pxl;
         const bool ok = lane_ok && p < nzp;
