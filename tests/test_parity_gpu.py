@@ -487,3 +487,54 @@ def test_context_orders_calls_across_streams():
     for d, gi in outs:
         assert float(d.item()) == D0
         assert torch.equal(gi, g0)
+
+
+@pytest.mark.parametrize("dims,K", [((62, 5), 3), ((64, 2), 4), ((126, 9), 5), ((130, 40), 40), ((2, 7), 3),
+                                    ((1024, 3), 2), ((190, 70), 70)])
+def test_ngf_fast_sampler_matches_generic(dims, K):
+    """k_ngf_sfeat2f (one warp per 62-column chunk and row segment, shuffles, rsqrt.approx) against the generic
+    k_ngf_sfeat2 (SEQREG_B200_SFEAT=0, read at launch) on ragged shapes: a single chunk, a chunk of 2 columns,
+    2- and 3-row images (every look-ahead row missing), several segments, K in each Gram bucket.  Same D to
+    1e-6 and the same gradient to 1e-5 of its max (rsqrt.approx is 2^-22 relative), and both match the oracle
+    at the fp32 tolerance."""
+    import os
+
+    rng = np.random.default_rng(11)
+    sp, org = (0.5, 0.25), (-3.0, 1.0)
+    from scipy.ndimage import gaussian_filter
+
+    frames = np.stack([gaussian_filter(rng.standard_normal(dims), 1.2, mode="reflect").ravel(order="F") + 2.0
+                       for _ in range(K)])
+    x = orc.cell_centers(dims, sp, org).T
+    y = x[None] + 0.35 * rng.standard_normal((K,) + x.shape) * np.asarray(sp)[None, :, None]
+    t_ = (y - np.asarray(org)[None, :, None]) / np.asarray(sp)[None, :, None] - 0.5
+    fr = t_ - np.floor(t_)
+    y = np.where((fr < 2e-3) | (fr > 1 - 2e-3), y + 5e-3 * np.asarray(sp)[None, :, None], y)
+    w = rng.uniform(0.5, 1.0, K)
+    h = float(np.prod(sp))
+    fd = _frames_dev(frames, dims, sp, org, torch.float32)
+    res = []
+    old = os.environ.get("SEQREG_B200_SFEAT")
+    try:
+        for flag in (None, "0"):
+            if flag is None:
+                os.environ.pop("SEQREG_B200_SFEAT", None)
+            else:
+                os.environ["SEQREG_B200_SFEAT"] = flag
+            obj = srb.FieldObjective(fd, list(range(K)), w, h, feature="ngf", ngf_eps=0.3)
+            yt = torch.as_tensor(y).to(device=fd.data.device, dtype=torch.float32).contiguous()
+            stats, g = obj.evaluate(yt)  # a fresh objective and iterate: the eager path, no graph replay
+            res.append((float(stats[0].item()), g.double().cpu().numpy().copy()))
+    finally:
+        if old is None:
+            os.environ.pop("SEQREG_B200_SFEAT", None)
+        else:
+            os.environ["SEQREG_B200_SFEAT"] = old
+    (Df, gf), (Dg, gg) = res
+    assert Df == pytest.approx(Dg, rel=1e-6)
+    assert np.abs(gf - gg).max() <= 1e-5 * np.abs(gg).max()
+    q = frames.astype(np.float32).astype(np.float64)
+    yq = y.astype(np.float32).astype(np.float64)
+    _, Dref, gref = orc.evaluate_field(list(q), dims, sp, org, yq, w, h, "ngf", 0.3)
+    assert Df == pytest.approx(Dref, rel=1e-4)
+    assert _relmax(gf, gref) < 1e-4

@@ -7,6 +7,7 @@ oracle's D and dD/dy: each variant runs the fp32 field parity cases in a fresh p
     SEQREG_B200_P2S=0     re-gathering pass 2 (default: streaming pass 2 from the split pass 1's V, grad T)
     SEQREG_B200_GRAPH=0   no CUDA-graph replay of repeated sr_evaluate calls
     SEQREG_B200_P2TMA=0   2-D NCC pass 2 loads straight from HBM (k_pass2_mma; default TMA-fed k_pass2_tma)
+    SEQREG_B200_SFEAT=0   2-D NGF: the generic fused sampler k_ngf_sfeat2 instead of k_ngf_sfeat2f
 
 (The round-1 variants measured slower — tcgen05 NCC pass 1 / pass 2, warp-specialized pass 2, fused
 sampling + Gram, texture gathers, PDL, the unpipelined sampler — were removed from the library.)
@@ -67,7 +68,7 @@ print(json.dumps(out))
 
 
 @pytest.mark.parametrize("env", ["SEQREG_B200_LEGACY=1", "SEQREG_B200_TC=0", "SEQREG_B200_P2S=0", "SEQREG_B200_GRAPH=0",
-                                 "SEQREG_B200_P2TMA=0", ""])
+                                 "SEQREG_B200_P2TMA=0", "SEQREG_B200_SFEAT=0", ""])
 def test_variant_parity(env):
     e = dict(os.environ)
     if env:
