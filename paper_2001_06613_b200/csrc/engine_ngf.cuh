@@ -291,17 +291,22 @@ static __device__ __forceinline__ void umma_h16(uint32_t tmem_d, uint64_t adesc,
 }
 struct TGH {
   // 16 splitter warps, 1 MMA issuer warp, 4 flusher warps (one per TMEM lane quarter), 1 TMA producer warp
-  static constexpr int NSP = 512, NT = NSP + 32 + 128 + 32, TP = 64;
-  static constexpr int NB = 3, NA = 2, R = 32, TS = 256, MAXST = 8;  // R tiles of 64 pixels per TMEM slot
+  static constexpr int NSP = 512, NT = NSP + 32 + 128 + 32;
+  static constexpr int NB = 3, NA = 2, RPX = 2048, TS = 256, MAXST = 8;  // RPX pixels per TMEM slot and flush
 };
+// A tile is natom K-atoms of 64 pixels (tp = 64 natom pixels of one component): 1 atom for more than 64
+// frames, 2 for 33..64, 4 for up to 32, so that a tile is 16-32 KB whatever the subset size (the per-tile
+// hand-offs, not the bytes, bound the kernel).  Operand buffer: [atom][H (rows); L (rows)][128 B].
 struct GhLayout {
-  int rows, sbytes, obytes, nst;
+  int rows, natom, tp, sbytes, obytes, nst;
 };
 inline GhLayout tgh_layout(int K, size_t smem_cap) {
   GhLayout L{};
   L.rows = (K + 15) / 16 * 16;
-  L.sbytes = L.rows * TGH::TP * 4;
-  L.obytes = 2 * L.rows * 128;
+  L.natom = L.rows <= 32 ? 4 : L.rows <= 64 ? 2 : 1;
+  L.tp = 64 * L.natom;
+  L.sbytes = L.rows * L.tp * 4;
+  L.obytes = L.natom * 2 * L.rows * 128;
   const size_t fixed = 1024 + (size_t)TGH::NB * L.obytes + 512;
   const int nst = smem_cap > fixed ? (int)((smem_cap - fixed) / L.sbytes) : 0;
   L.nst = nst > TGH::MAXST ? TGH::MAXST : nst;
@@ -319,8 +324,10 @@ template <int KP>  // KP = 64 or 128: the partial block layout [KP x KP | s | vm
 __global__ void __launch_bounds__(TGH::NT, 1) k_gram_h(const Args a, const __grid_constant__ CUtensorMap xmap,
                                                        int ntx, int ncomp, const GhLayout lay) {
   using C = TGH;
-  constexpr int TP = C::TP, NB = C::NB, NA = C::NA;
+  constexpr int NB = C::NB, NA = C::NA;
+  constexpr int NATOM = KP > 64 ? 1 : KP > 32 ? 2 : 4, TP = 64 * NATOM, R = C::RPX / TP;  // = lay.natom, lay.tp
   const int NST = lay.nst;
+  const uint32_t ATOMB = (uint32_t)(2 * lay.rows * 128);  // bytes of one K-atom of the [H; L] operand
   extern __shared__ __align__(1024) unsigned char smem_gh[];
   unsigned char* base = smem_gh + ((1024 - (smem_u32(smem_gh) & 1023)) & 1023);
   unsigned char* Vb = base;                                                      // [NB][2 rows][128 B] SW128
@@ -380,51 +387,59 @@ __global__ void __launch_bounds__(TGH::NT, 1) k_gram_h(const Args a, const __gri
     // The 4 f16 hi (and lo) of a lane are half a 16-byte operand chunk: 64-bit stores, a half-warp fills one
     // swizzled 128-byte operand row.
     const int hl = lane >> 4, cl = lane & 15;
-    const int r0 = 2 * warp + hl;  // rows r0 + 32 it
-    const uint32_t soff = (uint32_t)(r0 * TP + 4 * cl) * 4;                      // stage bytes, + 32 TP 4 per step
+    const int r0 = 2 * warp + hl;
+    // 4 steps per tile: step e = (row block e & (nrb - 1): rows r0 + 32 rbk, atom e >> log2(nrb)), nrb = 4 / NATOM
+    constexpr int nrb = 4 / NATOM, lrb = nrb == 4 ? 2 : nrb == 2 ? 1 : 0;
     const uint32_t ooff = (uint32_t)((r0 >> 3) * 1024 + (r0 & 7) * 128 + ((((cl >> 1) ^ r0) & 7) << 4) + (cl & 1) * 8);
-    const uint32_t loff = ooff + (uint32_t)KPN * 128;                            // L rows: KPN % 8 == 0
+    const uint32_t lrow = (uint32_t)KPN * 128;  // L rows: KPN % 8 == 0
     float fm[4] = {0.f, 0.f, 0.f, 0.f};
     int st = 0;
     uint32_t stph = 0;
     for (long long n = 0; n < nloc; ++n) {
       const int b = (int)(n % NB);
       mbar_wait(&st_full[st], stph);
-      const unsigned char* src = reinterpret_cast<const unsigned char*>(stage) + (size_t)st * lay.sbytes + soff;
+      const unsigned char* src = reinterpret_cast<const unsigned char*>(stage) + (size_t)st * lay.sbytes;
       uint2 hw[4], lw[4];
 #pragma unroll
-      for (int it = 0; it < 4; ++it) {
+      for (int e = 0; e < 4; ++e) {
+        const int rbk = e & (nrb - 1), at = e >> lrb, row = r0 + 32 * rbk;
         float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (r0 + 32 * it < KPN) q = *reinterpret_cast<const float4*>(src + it * (32 * TP * 4));
-        fm[it] = fmaxf(fm[it], fmaxf(fmaxf(fabsf(q.x), fabsf(q.y)), fmaxf(fabsf(q.z), fabsf(q.w))));
+        if (row < KPN) q = *reinterpret_cast<const float4*>(src + (size_t)(row * TP + at * 64 + 4 * cl) * 4);
+        fm[e] = fmaxf(fm[e], fmaxf(fmaxf(fabsf(q.x), fabsf(q.y)), fmaxf(fabsf(q.z), fabsf(q.w))));
         const __half2 h0 = __floats2half2_rn(q.x, q.y), h1 = __floats2half2_rn(q.z, q.w);
         const float2 f0 = __half22float2(h0), f1 = __half22float2(h1);
         const __half2 l0 = __floats2half2_rn(q.x - f0.x, q.y - f0.y), l1 = __floats2half2_rn(q.z - f1.x, q.w - f1.y);
-        hw[it] = make_uint2(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1));
-        lw[it] = make_uint2(*reinterpret_cast<const uint32_t*>(&l0), *reinterpret_cast<const uint32_t*>(&l1));
+        hw[e] = make_uint2(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1));
+        lw[e] = make_uint2(*reinterpret_cast<const uint32_t*>(&l0), *reinterpret_cast<const uint32_t*>(&l1));
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&st_free[st]);  // the stage is in registers: the producer may refill it
       if (n >= NB) mbar_wait(&vb_free[b], (uint32_t)((n / NB - 1) & 1));
       unsigned char* ob = Vb + (size_t)b * lay.obytes;
 #pragma unroll
-      for (int it = 0; it < 4; ++it)
-        if (r0 + 32 * it < KPN) {
-          *reinterpret_cast<uint2*>(ob + ooff + it * 4096) = hw[it];
-          *reinterpret_cast<uint2*>(ob + loff + it * 4096) = lw[it];
+      for (int e = 0; e < 4; ++e) {
+        const int rbk = e & (nrb - 1), at = e >> lrb;
+        if (r0 + 32 * rbk < KPN) {
+          unsigned char* dst = ob + (uint32_t)at * ATOMB + ooff + (uint32_t)rbk * 4096;
+          *reinterpret_cast<uint2*>(dst) = hw[e];
+          *reinterpret_cast<uint2*>(dst + lrow) = lw[e];
         }
+      }
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&vb_full[b]);
       if (++st == NST) st = 0, stph ^= 1;
     }
+    // max |n| per row: the steps of a row block (one per atom) share the row
+    if (nrb == 2) fm[0] = fmaxf(fm[0], fm[2]), fm[1] = fmaxf(fm[1], fm[3]);
+    if (nrb == 1) fm[0] = fmaxf(fmaxf(fm[0], fm[1]), fmaxf(fm[2], fm[3]));
 #pragma unroll
     for (int it = 0; it < 4; ++it) {
       float v = fm[it];
 #pragma unroll
       for (int o = 1; o < 16; o <<= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
       const int r = r0 + 32 * it;
-      if (cl == 0 && r < KP) {
+      if (cl == 0 && r < KP && it < nrb) {
         out[KP * KP + r] = 0.0;  // s: unused by NGF
         out[KP * KP + KP + r] = r < K ? (double)v : 0.0;
         out[KP * KP + 2 * KP + r] = r < K ? (double)v : 0.0;
@@ -435,19 +450,20 @@ __global__ void __launch_bounds__(TGH::NT, 1) k_gram_h(const Args a, const __gri
     if (lane == 0) {
       const uint32_t idesc = umma_idesc_h16(128, 2 * KPN);
       for (long long n = 0; n < nloc; ++n) {
-        const long long grp = n / C::R;
-        const bool first = n % C::R == 0, last = n % C::R == C::R - 1 || n == nloc - 1;
+        const long long grp = n / R;
+        const bool first = n % R == 0, last = n % R == R - 1 || n == nloc - 1;
         const int b = (int)(n % NB), s = (int)(grp % NA);
         mbar_wait(&vb_full[b], (uint32_t)((n / NB) & 1));
         if (first && grp >= NA) mbar_wait(&acc_free[s], (uint32_t)((grp / NA - 1) & 1));
         tc_fence_after();
         const uint32_t o0 = smem_u32(Vb + (size_t)b * lay.obytes);
         const uint32_t acc = tmem + (uint32_t)(s * C::TS);
+        for (int at = 0; at < NATOM; ++at)
 #pragma unroll
-        for (int k16 = 0; k16 < TP / 16; ++k16) {
-          const uint64_t dh = umma_sdesc_sw128(o0 + (uint32_t)(k16 * 32));
-          umma_h16(acc, dh, dh, idesc, (k16 > 0 || !first) ? 1u : 0u);  // A = H (128 rows), B = [H; L]
-        }
+          for (int k16 = 0; k16 < 4; ++k16) {
+            const uint64_t dh = umma_sdesc_sw128(o0 + (uint32_t)at * ATOMB + (uint32_t)(k16 * 32));
+            umma_h16(acc, dh, dh, idesc, (at > 0 || k16 > 0 || !first) ? 1u : 0u);  // A = H (128 rows), B = [H; L]
+          }
         umma_commit(&vb_free[b]);
         if (last) umma_commit(&acc_full[s]);
       }
@@ -473,7 +489,7 @@ __global__ void __launch_bounds__(TGH::NT, 1) k_gram_h(const Args a, const __gri
     const int q = warp & 3, m = 32 * q + lane;
     const bool mok = m < KPN;  // TMEM lanes past KPN carry garbage rows (not accumulated)
     double* acol = out + (mok ? m : 0);
-    const long long ngrp = (nloc + C::R - 1) / C::R;
+    const long long ngrp = (nloc + R - 1) / R;
     for (long long n = 0; n < ngrp; ++n) {
       const int s = (int)(n % NA);
       mbar_wait(&acc_full[s], (uint32_t)((n / NA) & 1));

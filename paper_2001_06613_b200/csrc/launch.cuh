@@ -219,33 +219,64 @@ inline cudaError_t ngf_sfeat_d2(const Launch& L, const Args& a, const NgfBufs& B
   return cudaGetLastError();
 }
 
-template <int D, int KP>
-cudaError_t run_ngf_pass1_kp(const Launch& L, const Args& a, const NgfBufs& B, double* part, size_t part_cap,
-                             int* nblk) {
+// k_gram_h over the slab of Nf [K][D][zstride]: [KPN frames x tp pixels] fp32 boxes of one component, zero fill
+// past K and past the slab.  gram_h_prepare before the sampling kernels (NotSupported -> generic path).
+struct GramH {
+  GhLayout gl;
+  size_t smem;
+  CUtensorMap map;
+};
+template <int D>
+inline cudaError_t gram_h_prepare(const Args& a, const NgfBufs& B, GramH* g) {
   const long long npix = a.pix_hi - a.pix_lo;
-  if (npix <= 0 || a.K > KP) return cudaErrorNotSupported;
+  if (npix <= 0) return cudaErrorNotSupported;
   if (((a.pix_lo - B.zlo) * 4) % 16 || (B.zstride * 4) % 16 || (reinterpret_cast<uintptr_t>(B.Nf) & 15))
     return cudaErrorNotSupported;
   EncodeTiledFn fn = encode_tiled_fn();
   if (!fn) return cudaErrorNotSupported;
   int smem_cap = 0;
   cudaDeviceGetAttribute(&smem_cap, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0);
-  // k_gram_h: [KPN frames x 64 pixels] fp32 boxes of one component of Nf [K][D][zstride], zero fill past K and
-  // past the slab
-  const GhLayout gl = tgh_layout(a.K, (size_t)smem_cap);
-  const size_t hsm = tgh_smem(gl);
-  CUtensorMap hmap;
-  memset(&hmap, 0, sizeof hmap);
+  g->gl = tgh_layout(a.K, (size_t)smem_cap);
+  g->smem = tgh_smem(g->gl);
+  memset(&g->map, 0, sizeof g->map);
   cuuint64_t gdim[3] = {(cuuint64_t)npix, (cuuint64_t)D, (cuuint64_t)a.K};
   cuuint64_t gstr[2] = {(cuuint64_t)B.zstride * 4, (cuuint64_t)D * B.zstride * 4};
-  cuuint32_t hbox[3] = {(cuuint32_t)TGH::TP, 1, (cuuint32_t)gl.rows};
+  cuuint32_t hbox[3] = {(cuuint32_t)g->gl.tp, 1, (cuuint32_t)g->gl.rows};
   cuuint32_t es[3] = {1, 1, 1};
-  if (gl.nst < 2 || hsm > (size_t)smem_cap || 2 * gl.rows > 256 ||
-      fn(&hmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, B.Nf + (a.pix_lo - B.zlo), gdim, gstr, hbox, es,
+  if (g->gl.nst < 2 || g->smem > (size_t)smem_cap || 2 * g->gl.rows > 256 ||
+      fn(&g->map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, B.Nf + (a.pix_lo - B.zlo), gdim, gstr, hbox, es,
          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorNotSupported;
-  cudaError_t e = D == 2 ? ngf_sfeat_d2(L, a, B) : cudaErrorNotSupported;
+  return cudaSuccess;
+}
+template <int D, int KP>
+inline cudaError_t gram_h_launch(const Launch& L, const Args& a, const GramH& g, double* part, size_t part_cap,
+                                 int* nblk) {
+  const long long npix = a.pix_hi - a.pix_lo;
+  cudaError_t e = cudaFuncSetAttribute(k_gram_h<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
+  if (e != cudaSuccess) return e;
+  const int ntx = (int)((npix + g.gl.tp - 1) / g.gl.tp);
+  const long long ntiles = (long long)ntx * D;
+  int grid = L.grid_override > 0 ? L.grid_override : L.sms;
+  if (grid > ntiles) grid = (int)ntiles;
+  const size_t stride = (size_t)KP * KP + 3 * KP;
+  if ((size_t)grid * stride > part_cap) grid = (int)(part_cap / stride);
+  Args b = a;
+  b.part = part;
+  k_gram_h<KP><<<grid, TGH::NT, g.smem, L.stream>>>(b, g.map, ntx, D, g.gl);
+  *nblk = grid;
+  return cudaGetLastError();
+}
+
+template <int D, int KP>
+cudaError_t run_ngf_pass1_kp(const Launch& L, const Args& a, const NgfBufs& B, double* part, size_t part_cap,
+                             int* nblk) {
+  if (a.K > KP) return cudaErrorNotSupported;
+  GramH gh;
+  cudaError_t e = gram_h_prepare<D>(a, B, &gh);
+  if (e != cudaSuccess) return e;
+  e = D == 2 ? ngf_sfeat_d2(L, a, B) : cudaErrorNotSupported;
   if (e == cudaErrorNotSupported) {
     // u (an fp32 pair) and grad T over [vlo, vhi) (no shift: n only sees differences of u), then n, 1/rho
     Args av = a;
@@ -260,19 +291,7 @@ cudaError_t run_ngf_pass1_kp(const Launch& L, const Args& a, const NgfBufs& B, d
     e = cudaGetLastError();
   }
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_gram_h<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
-  if (e != cudaSuccess) return e;
-  const int ntx = (int)((npix + TGH::TP - 1) / TGH::TP);
-  const long long ntiles = (long long)ntx * D;
-  int grid = L.grid_override > 0 ? L.grid_override : L.sms;
-  if (grid > ntiles) grid = (int)ntiles;
-  const size_t stride = (size_t)KP * KP + 3 * KP;
-  if ((size_t)grid * stride > part_cap) grid = (int)(part_cap / stride);
-  Args b = a;
-  b.part = part;
-  k_gram_h<KP><<<grid, TGH::NT, hsm, L.stream>>>(b, hmap, ntx, D, gl);
-  *nblk = grid;
-  return cudaGetLastError();
+  return gram_h_launch<D, KP>(L, a, gh, part, part_cap, nblk);
 }
 
 template <int D>

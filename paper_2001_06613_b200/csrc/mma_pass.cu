@@ -63,17 +63,25 @@ static bool encode_p2g_map(EncodeTiledFn fn, CUtensorMap* m, const float* base, 
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// split NGF pass 1 for K <= 32: sampling, features, then the TMA-fed mma.sync Gram of n (KP = 32 partials)
+// split NGF pass 1 for K <= 32: sampling, features, then k_gram_h (tcgen05 kind::f16, 256-pixel tiles) with
+// KP = 32 partials; SEQREG_B200_GRAM32=0: the TMA-fed mma.sync Gram k_gram_tma<NGF> it replaced
 template <int D>
 static cudaError_t run_ngf_pass1_mma(const Launch& L, const Args& a, const NgfBufs& B, double* part,
                                      size_t part_cap, int* nblk) {
   const long long npix = a.pix_hi - a.pix_lo;
   if (npix <= 0 || a.K > GTM::KP) return cudaErrorNotSupported;
   if (((a.pix_lo - B.zlo) * 4) % 16) return cudaErrorNotSupported;
-  EncodeTiledFn fn = encode_tiled_fn();
+  static const bool use_h = !(getenv("SEQREG_B200_GRAM32") && getenv("SEQREG_B200_GRAM32")[0] == '0');
+  GramH gh;
   CUtensorMap xmap;
-  if (!fn || !encode_gram_map(fn, &xmap, B.Nf + (a.pix_lo - B.zlo), npix, D, a.K, B.zstride))
-    return cudaErrorNotSupported;
+  if (use_h) {
+    const cudaError_t eh = gram_h_prepare<D>(a, B, &gh);
+    if (eh != cudaSuccess) return eh;
+  } else {
+    EncodeTiledFn fn = encode_tiled_fn();
+    if (!fn || !encode_gram_map(fn, &xmap, B.Nf + (a.pix_lo - B.zlo), npix, D, a.K, B.zstride))
+      return cudaErrorNotSupported;
+  }
   Args av = a;  // u and grad T over [vlo, vhi) (no shift: n only sees differences of u)
   av.pix_lo = B.vlo;
   av.pix_hi = B.vhi;
@@ -88,6 +96,7 @@ static cudaError_t run_ngf_pass1_mma(const Launch& L, const Args& a, const NgfBu
     e = cudaGetLastError();
   }
   if (e != cudaSuccess) return e;
+  if (use_h) return gram_h_launch<D, 32>(L, a, gh, part, part_cap, nblk);
   const size_t smem = gtm_smem();
   auto gk = k_gram_tma<true>;
   e = cudaFuncSetAttribute(gk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
