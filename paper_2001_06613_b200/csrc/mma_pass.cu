@@ -64,29 +64,19 @@ static bool encode_p2g_map(EncodeTiledFn fn, CUtensorMap* m, const float* base, 
 }
 
 // split NGF pass 1 for K <= 32: sampling, features, then k_gram_h (tcgen05 kind::f16, 256-pixel tiles) with
-// KP = 32 partials; SEQREG_B200_GRAM32=0: the TMA-fed mma.sync Gram k_gram_tma<NGF> it replaced
+// KP = 32 partials (it replaced the TMA-fed mma.sync Gram k_gram_tma<NGF>: C4 0.23 -> 0.17 ms)
 template <int D>
 static cudaError_t run_ngf_pass1_mma(const Launch& L, const Args& a, const NgfBufs& B, double* part,
                                      size_t part_cap, int* nblk) {
-  const long long npix = a.pix_hi - a.pix_lo;
-  if (npix <= 0 || a.K > GTM::KP) return cudaErrorNotSupported;
-  if (((a.pix_lo - B.zlo) * 4) % 16) return cudaErrorNotSupported;
-  static const bool use_h = !(getenv("SEQREG_B200_GRAM32") && getenv("SEQREG_B200_GRAM32")[0] == '0');
+  if (a.K > 32) return cudaErrorNotSupported;
   GramH gh;
-  CUtensorMap xmap;
-  if (use_h) {
-    const cudaError_t eh = gram_h_prepare<D>(a, B, &gh);
-    if (eh != cudaSuccess) return eh;
-  } else {
-    EncodeTiledFn fn = encode_tiled_fn();
-    if (!fn || !encode_gram_map(fn, &xmap, B.Nf + (a.pix_lo - B.zlo), npix, D, a.K, B.zstride))
-      return cudaErrorNotSupported;
-  }
+  cudaError_t e = gram_h_prepare<D>(a, B, &gh);
+  if (e != cudaSuccess) return e;
   Args av = a;  // u and grad T over [vlo, vhi) (no shift: n only sees differences of u)
   av.pix_lo = B.vlo;
   av.pix_hi = B.vhi;
   av.shifts = nullptr;
-  cudaError_t e = D == 2 ? ngf_sfeat_d2(L, a, B) : cudaErrorNotSupported;
+  e = D == 2 ? ngf_sfeat_d2(L, a, B) : cudaErrorNotSupported;
   if (e == cudaErrorNotSupported) {
     e = launch_sample_vg<D>(L, av, B.V, B.G, B.vstride, B.VL);
     if (e != cudaSuccess) return e;
@@ -96,20 +86,7 @@ static cudaError_t run_ngf_pass1_mma(const Launch& L, const Args& a, const NgfBu
     e = cudaGetLastError();
   }
   if (e != cudaSuccess) return e;
-  if (use_h) return gram_h_launch<D, 32>(L, a, gh, part, part_cap, nblk);
-  const size_t smem = gtm_smem();
-  auto gk = k_gram_tma<true>;
-  e = cudaFuncSetAttribute(gk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  const int ntx = (int)((npix + GTM::TP - 1) / GTM::TP);
-  int grid = occupancy_grid(L, gk, GTM::NT, smem, (long long)ntx * D);
-  const size_t stride = (size_t)GTM::KP * GTM::KP + 3 * GTM::KP;
-  if ((size_t)grid * stride > part_cap) grid = (int)(part_cap / stride);
-  Args b = a;
-  b.part = part;
-  gk<<<grid, GTM::NT, smem, L.stream>>>(b, xmap, ntx);
-  *nblk = grid;
-  return cudaGetLastError();
+  return gram_h_launch<D, 32>(L, a, gh, part, part_cap, nblk);
 }
 cudaError_t ngf_pass1_mma_d2(const Launch& L, const Args& a, const NgfBufs& B, double* part, size_t cap, int* nblk) {
   return run_ngf_pass1_mma<2>(L, a, B, part, cap, nblk);

@@ -1,6 +1,6 @@
 """Small evaluations through every default kernel family, for compute-sanitizer (tests/test_sanitizer_gpu.py):
 fp32 NCC K = 24 (k_sample_vp, k_gram_tma, k_reduce_finalize, k_pass2_tma), fp32 NGF K = 40 and K = 100
-(k_ngf_sfeat2, k_gram_h<64|128>, k_ngf_z_tc), fp32 NGF K = 20 (k_gram_tma<NGF>, k_ngf_z_f16), 3-D fp32 NGF,
+(k_ngf_sfeat2f, k_gram_h<64|128>, k_ngf_z_tc), fp32 NGF K = 20 (k_gram_h<32>, k_ngf_z_f16), 3-D fp32 NGF,
 fp64 NGF (generic kernels), the fused curvature (sr_evaluate_reg) and a 129-frame subset (frame blocks)."""
 
 import sys
