@@ -27,4 +27,4 @@ def test_bench_algorithmic_bytes():
 
     assert bench.bytes_per_vf(2, 4)["eval"] == 32 and bench.bytes_per_vf(3, 4)["eval"] == 44
     kb = bench.kernel_bytes_per_vf(2, 4)["algorithmic"]
-    assert kb["k_ngf_sfeat2"] + kb["k_ngf_adj4"] == 32
+    assert kb["k_ngf_sfeat2f"] + kb["k_ngf_adj4"] == 32 and kb["k_ngf_sfeat2"] == kb["k_ngf_sfeat2f"]
