@@ -47,37 +47,43 @@ __global__ void __launch_bounds__(256) k_ngf_feat4(const Args a, const float* __
   coords_flat(a.g, p0, c);
   const float e = (float)a.eps;
   float nv[D][4], rv[4];
-  // interior fast path: the 4 pixels share their row and every axis index stays in 1 .. n - 2 (central
-  // differences everywhere); the u rows come as 128-bit loads
-  // (2-D only: with 128-pixel 3-D rows every warp holds a boundary thread and would run both paths)
-  bool inner = D == 2 && q0 + 4 <= nz && c[0] >= 1 && c[0] + 3 <= a.g.n[0] - 2 && ((zlo - vlo + q0) & 3) == 0 &&
-               (vstride & 3) == 0 && (reinterpret_cast<uintptr_t>(V) & 15) == 0;
+  // vector path: the 4 pixels share their row (n0 % 4 == 0, aligned ranges); the u rows come as 128-bit loads.
+  // Domain edges are handled without a second path (a 128-pixel 3-D row puts a boundary thread in every
+  // warp): the neighbour index is clamped (u(-1) := u(0): the one-sided difference) and the factor is 1/s
+  // instead of 1/(2 s) there; the same expressions as the per-pixel path below, so the same bits.
+  bool inner = q0 + 4 <= nz && (a.g.n[0] & 3) == 0 && ((zlo | vlo) & 3) == 0 && (vstride & 3) == 0 &&
+               ((reinterpret_cast<uintptr_t>(V) | reinterpret_cast<uintptr_t>(VL)) & 15) == 0;
 #pragma unroll
-  for (int ax = 1; ax < D; ++ax) inner = inner && c[ax] >= 1 && c[ax] <= a.g.n[ax] - 2 && (a.g.sti[ax] & 3) == 0;
+  for (int ax = 1; ax < D; ++ax) inner = inner && (a.g.sti[ax] & 3) == 0;
   if (inner) {
     float g4[D][4];
 #pragma unroll
     for (int ax = 0; ax < D; ++ax) {
-      float um[4], up[4], dl[4];
+      float um[4], up[4], dl[4], f[4];
+      const float inv = a.g.invf[ax];
       if (ax == 0) {
+        const bool hm = c[0] > 0, hp = c[0] + 3 < a.g.n[0] - 1;  // the row continues to the left / right
         const float4 u0 = __ldg(reinterpret_cast<const float4*>(u + q0));
-        um[0] = __ldg(u + q0 - 1), um[1] = u0.x, um[2] = u0.y, um[3] = u0.z;
-        up[0] = u0.y, up[1] = u0.z, up[2] = u0.w, up[3] = __ldg(u + q0 + 4);
+        um[0] = hm ? __ldg(u + q0 - 1) : u0.x, um[1] = u0.x, um[2] = u0.y, um[3] = u0.z;
+        up[0] = u0.y, up[1] = u0.z, up[2] = u0.w, up[3] = hp ? __ldg(u + q0 + 4) : u0.w;
         const float4 l0 = __ldg(reinterpret_cast<const float4*>(ul + q0));
-        dl[0] = l0.y - __ldg(ul + q0 - 1), dl[1] = l0.z - l0.x, dl[2] = l0.w - l0.y, dl[3] = __ldg(ul + q0 + 4) - l0.z;
+        dl[0] = l0.y - (hm ? __ldg(ul + q0 - 1) : l0.x), dl[1] = l0.z - l0.x, dl[2] = l0.w - l0.y;
+        dl[3] = (hp ? __ldg(ul + q0 + 4) : l0.w) - l0.z;
+        f[0] = hm ? inv * 0.5f : inv, f[1] = f[2] = inv * 0.5f, f[3] = hp ? inv * 0.5f : inv;
       } else {
-        const int st = a.g.sti[ax];
-        const float4 m4 = __ldg(reinterpret_cast<const float4*>(u + q0 - st));
-        const float4 p4 = __ldg(reinterpret_cast<const float4*>(u + q0 + st));
+        const bool hm = c[ax] > 0, hp = c[ax] < a.g.n[ax] - 1;
+        const int st = a.g.sti[ax], sm = hm ? st : 0, sp = hp ? st : 0;
+        const float4 m4 = __ldg(reinterpret_cast<const float4*>(u + q0 - sm));
+        const float4 p4 = __ldg(reinterpret_cast<const float4*>(u + q0 + sp));
         um[0] = m4.x, um[1] = m4.y, um[2] = m4.z, um[3] = m4.w;
         up[0] = p4.x, up[1] = p4.y, up[2] = p4.z, up[3] = p4.w;
-        const float4 lm = __ldg(reinterpret_cast<const float4*>(ul + q0 - st));
-        const float4 lp = __ldg(reinterpret_cast<const float4*>(ul + q0 + st));
+        const float4 lm = __ldg(reinterpret_cast<const float4*>(ul + q0 - sm));
+        const float4 lp = __ldg(reinterpret_cast<const float4*>(ul + q0 + sp));
         dl[0] = lp.x - lm.x, dl[1] = lp.y - lm.y, dl[2] = lp.z - lm.z, dl[3] = lp.w - lm.w;
+        f[0] = f[1] = f[2] = f[3] = (hm && hp) ? inv * 0.5f : inv;
       }
-      const float inv = a.g.invf[ax];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) g4[ax][t] = ((up[t] - um[t]) + dl[t]) * (inv * 0.5f);
+      for (int t = 0; t < 4; ++t) g4[ax][t] = ((up[t] - um[t]) + dl[t]) * f[t];
     }
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
