@@ -145,6 +145,19 @@ __global__ void __launch_bounds__(256) k_ngf_feat4(const Args a, const float* __
 // CURV (sr_evaluate_reg): the curvature gradient alpha h L L (y - x) of the same pixels is added to the
 // output in the same launch (same arithmetic and the same float addition as k_curvature after this kernel),
 // and the CTA's share of S goes to a.curv_part[blockIdx.y * gridDim.x + blockIdx.x].
+// (D_h^T z) terms of one axis at index i of n: rows i - 1, i + 1 (interior) and the one-sided edge rows
+// (dgrad_adjoint); zm, z0, zp = z at i - 1, i, i + 1 (any finite value where the row does not exist)
+__device__ __forceinline__ float adj_terms(int i, int n, float zm, float z0, float zp, float h2, float inv) {
+  float o = 0.f;
+  if (i - 1 >= 1 && i - 1 <= n - 2) o += zm * h2;
+  if (i + 1 >= 1 && i + 1 <= n - 2) o -= zp * h2;
+  if (i == 0) o -= z0 * inv;
+  if (i == 1) o += zm * inv;
+  if (i == n - 1) o += z0 * inv;
+  if (i == n - 2) o -= zp * inv;
+  return o;
+}
+
 template <int D, bool CURV = false>
 __global__ void __launch_bounds__(256) k_ngf_adj4(const Args a, const float* __restrict__ Z, long long zlo,
                                                   long long zstride, const float* __restrict__ Gv, long long vlo,
@@ -159,6 +172,43 @@ __global__ void __launch_bounds__(256) k_ngf_adj4(const Args a, const float* __r
   int c[3];
   coords_flat(a.g, p0, c);
   float du[4];
+  // vector path: the 4 pixels share their row; the z rows come as 128-bit loads with clamped row / column
+  // offsets at the domain edges (no second path: a 128-pixel 3-D row puts a boundary thread in every warp),
+  // and adj_terms applies the per-pixel edge rules: the per-pixel path's expressions, so the same bits
+  bool inner3 = D == 3 && q0 + 4 <= npix && (a.g.n[0] & 3) == 0 && (c[0] & 3) == 0 && ((p0 - zlo) & 3) == 0 &&
+               (zstride & 3) == 0 && (reinterpret_cast<uintptr_t>(Z) & 15) == 0;
+#pragma unroll
+  for (int ax = 1; ax < D; ++ax) inner3 = inner3 && (a.g.sti[ax] & 3) == 0;
+  if (inner3) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) du[t] = 0.f;
+#pragma unroll
+    for (int ax = 0; ax < D; ++ax) {
+      const float* z = Z + ((long long)k * D + ax) * zstride + (p0 - zlo);
+      const float inv = a.g.invf[ax], h2 = inv * 0.5f;
+      const int n = a.g.n[ax];
+      float zm[4], zp[4], z0[4];
+      if (ax == 0) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(z));
+        z0[0] = v.x, z0[1] = v.y, z0[2] = v.z, z0[3] = v.w;
+        zm[0] = c[0] > 0 ? __ldg(z - 1) : v.x, zm[1] = v.x, zm[2] = v.y, zm[3] = v.z;
+        zp[0] = v.y, zp[1] = v.z, zp[2] = v.w, zp[3] = c[0] + 4 < n ? __ldg(z + 4) : v.w;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) du[t] += adj_terms(c[0] + t, n, zm[t], z0[t], zp[t], h2, inv);
+      } else {
+        const int i = c[ax], st = a.g.sti[ax];
+        const float4 m4 = __ldg(reinterpret_cast<const float4*>(z - (i > 0 ? st : 0)));
+        const float4 p4 = __ldg(reinterpret_cast<const float4*>(z + (i < n - 1 ? st : 0)));
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (i == 0 || i == n - 1) v = __ldg(reinterpret_cast<const float4*>(z));
+        zm[0] = m4.x, zm[1] = m4.y, zm[2] = m4.z, zm[3] = m4.w;
+        zp[0] = p4.x, zp[1] = p4.y, zp[2] = p4.z, zp[3] = p4.w;
+        z0[0] = v.x, z0[1] = v.y, z0[2] = v.z, z0[3] = v.w;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) du[t] += adj_terms(i, n, zm[t], z0[t], zp[t], h2, inv);
+      }
+    }
+  } else {
   // interior fast path: the 4 pixels share their row and every axis index stays in 2 .. n - 3, so
   // (D_h^T z)(p) = sum_ax (z[p - st] - z[p + st]) h / 2; the z rows come as 128-bit loads
   // (2-D only, as in k_ngf_feat4)
@@ -220,6 +270,7 @@ __global__ void __launch_bounds__(256) k_ngf_adj4(const Args a, const float* __r
       }
     }
   }
+  }  // !inner3
   float* out = reinterpret_cast<float*>(a.out);
   const long long go = (long long)(p0 - vlo), oo = (long long)p0 - a.o_off;
   const bool vec = q0 + 4 <= npix && ((go | vstride) & 3) == 0 && ((oo | a.o_stride) & 3) == 0 &&
