@@ -847,11 +847,15 @@ struct CornersF {
   float v00, v10, v01, v11, f0, f1;
   bool inside;
 };
-template <int PF>
+// iv0, iv1: 1 / spacing when POW2 (exact; t = (p - o) (1/s) - 0.5 in one FMA), else the spacing itself
+// (t = (p - o) / s - 0.5 with the true division of grid.py:199-233, as interp2_prep)
+template <int PF, bool POW2>
 __device__ __forceinline__ CornersF fetch2f(const float* __restrict__ img, float of0, float of1, float iv0, float iv1,
                                             float hi0, float hi1, int m0, int m1, int s1, float px, float py) {
   CornersF c;
-  const float t0 = fmaf(__fsub_rn(px, of0), iv0, -0.5f), t1 = fmaf(__fsub_rn(py, of1), iv1, -0.5f);
+  const float q0 = __fsub_rn(px, of0), q1 = __fsub_rn(py, of1);
+  const float t0 = POW2 ? fmaf(q0, iv0, -0.5f) : __fsub_rn(__fdiv_rn(q0, iv0), 0.5f);
+  const float t1 = POW2 ? fmaf(q1, iv1, -0.5f) : __fsub_rn(__fdiv_rn(q1, iv1), 0.5f);
   const float c0 = fminf(fmaxf(t0, 0.f), hi0), c1 = fminf(fmaxf(t1, 0.f), hi1);
   c.inside = (c0 == t0) && (c1 == t1);
   const int i0 = min(__float2int_rz(c0), m0), i1 = min(__float2int_rz(c1), m1);  // c >= 0: trunc = floor
@@ -866,18 +870,19 @@ __device__ __forceinline__ CornersF fetch2f(const float* __restrict__ img, float
     asm volatile("prefetch.global.L2 [%0];" ::"l"(q + min(PF, m1 + 1 - i1) * s1));
   return c;
 }
+template <bool POW2>
 __device__ __forceinline__ double finish2f(const CornersF& c, float iv0, float iv1, float& g0, float& g1) {
   const float d0 = c.v10 - c.v00, d1 = c.v11 - c.v01;
   const float a0f = fmaf(c.f0, d0, c.v00), a1f = fmaf(c.f0, d1, c.v01);
   const float gv0 = fmaf(c.f1, d1 - d0, d0), gv1 = a1f - a0f;
-  g0 = c.inside ? gv0 * iv0 : 0.f;
-  g1 = c.inside ? gv1 * iv1 : 0.f;
+  g0 = c.inside ? (POW2 ? gv0 * iv0 : __fdiv_rn(gv0, iv0)) : 0.f;
+  g1 = c.inside ? (POW2 ? gv1 * iv1 : __fdiv_rn(gv1, iv1)) : 0.f;
   const double a0 = fma((double)c.f0, (double)c.v10 - (double)c.v00, (double)c.v00);
   const double a1 = fma((double)c.f0, (double)c.v11 - (double)c.v01, (double)c.v01);
   return c.inside ? fma((double)c.f1, a1 - a0, a0) : 0.0;
 }
 
-template <int MINB>
+template <int MINB, bool POW2>
 __global__ void __launch_bounds__(32, MINB) k_ngf_sfeat2f(
     const Args a, int seg, int rz0, int rz1, int rs0, int rs1, float* __restrict__ Nf,
     float* __restrict__ IRho, long long zlo, long long zstride, float* __restrict__ Gv, long long vlo,
@@ -905,12 +910,17 @@ __global__ void __launch_bounds__(32, MINB) k_ngf_sfeat2f(
   asm volatile("" : "+l"(img), "+l"(y0b), "+l"(g0b), "+l"(n0b), "+l"(irb_));
   const unsigned ys = (unsigned)a.y_stride, vs = (unsigned)vstride, zs = (unsigned)zstride;
   const unsigned dx1 = (unsigned)(xs1 - xs0);  // 0 on a clamped column, else 1
-  const float of0 = a.g.of[0], of1 = a.g.of[1], iv0 = a.g.invf[0], iv1 = a.g.invf[1];
+  const float of0 = a.g.of[0], of1 = a.g.of[1];
+  const float iv0 = POW2 ? a.g.invf[0] : a.g.sf[0], iv1 = POW2 ? a.g.invf[1] : a.g.sf[1];  // see fetch2f
   const float hi0 = (float)(n0 - 1), hi1 = (float)(n1 - 1);
   const int m0 = n0 - 2, m1 = n1 - 2, s1 = a.g.sti[1];
   const float e = (float)a.eps, e2 = e * e;
-  // stencil factors: central 1/(2 s) inside, one-sided 1/s on the first / last column and row
-  const float fxa = (xa > 0 && xa < n0 - 1) ? 0.5f * iv0 : iv0, fxb = (xa + 1 > 0 && xa + 1 < n0 - 1) ? 0.5f * iv0 : iv0;
+  // stencil factors: central 1/(2 s) inside, one-sided 1/s on the first / last column and row.  POW2: applied
+  // in fp32 after the rounding of the fp64 difference (a power of two commutes with the rounding); else in
+  // fp64 before it, as k_ngf_sfeat2 / ngf_at do.
+  const bool ina = xa > 0 && xa < n0 - 1, inb = xa + 1 > 0 && xa + 1 < n0 - 1;
+  const float fxa = ina ? 0.5f * a.g.invf[0] : a.g.invf[0], fxb = inb ? 0.5f * a.g.invf[0] : a.g.invf[0];
+  const double dxa = ina ? 0.5 * a.g.inv[0] : a.g.inv[0], dxb = inb ? 0.5 * a.g.inv[0] : a.g.inv[0];
   const int glo = max(ra, rs0), ghi = min(rb, rs1);  // rows whose grad T this segment writes
   const int rlast = min(rb, n1 - 1);                 // last row this segment samples
 
@@ -930,13 +940,13 @@ __global__ void __launch_bounds__(32, MINB) k_ngf_sfeat2f(
     asm volatile("prefetch.global.L2 [%0];" ::"l"(y0b + (q + ys)));
   };
   auto fetch = [&]() {
-    ca = fetch2f<PT>(img, of0, of1, iv0, iv1, hi0, hi1, m0, m1, s1, ya0, ya1);
-    cb = fetch2f<0>(img, of0, of1, iv0, iv1, hi0, hi1, m0, m1, s1, yb0, yb1);
+    ca = fetch2f<PT, POW2>(img, of0, of1, iv0, iv1, hi0, hi1, m0, m1, s1, ya0, ya1);
+    cb = fetch2f<0, POW2>(img, of0, of1, iv0, iv1, hi0, hi1, m0, m1, s1, yb0, yb1);
   };
   auto finish = [&](int r, unsigned q, double (&u)[2]) {
     float g0a, g1a, g0c, g1c;
-    u[0] = finish2f(ca, iv0, iv1, g0a, g1a);
-    u[1] = finish2f(cb, iv0, iv1, g0c, g1c);
+    u[0] = finish2f<POW2>(ca, iv0, iv1, g0a, g1a);
+    u[1] = finish2f<POW2>(cb, iv0, iv1, g0c, g1c);
     if (r >= glo && r < ghi) {  // warp-uniform
       const float g0n = __shfl_down_sync(0xffffffffu, g0a, 1), g1n = __shfl_down_sync(0xffffffffu, g1a, 1);
       if (st_ok) {
@@ -949,11 +959,19 @@ __global__ void __launch_bounds__(32, MINB) k_ngf_sfeat2f(
   auto step = [&](auto tailc, int r, unsigned q, double (&um)[2], const double (&uc)[2], const double (&up)[2]) {
     constexpr bool TAIL = decltype(tailc)::value;
     const double left = __shfl_up_sync(0xffffffffu, uc[1], 1), right = __shfl_down_sync(0xffffffffu, uc[0], 1);
-    const float fy = (r > 0 && r + 1 < n1) ? 0.5f * iv1 : iv1;
+    const bool iny = r > 0 && r + 1 < n1;
     double uq0 = up[0], uq1 = up[1];
     if (TAIL && r + 1 >= n1) uq0 = uc[0], uq1 = uc[1];  // u(n1) := u(n1 - 1)
-    const float gxa = (float)(uc[1] - left) * fxa, gxb = (float)(right - uc[0]) * fxb;
-    const float gya = (float)(uq0 - um[0]) * fy, gyb = (float)(uq1 - um[1]) * fy;
+    float gxa, gxb, gya, gyb;
+    if (POW2) {
+      const float fy = iny ? 0.5f * a.g.invf[1] : a.g.invf[1];
+      gxa = (float)(uc[1] - left) * fxa, gxb = (float)(right - uc[0]) * fxb;
+      gya = (float)(uq0 - um[0]) * fy, gyb = (float)(uq1 - um[1]) * fy;
+    } else {
+      const double dy = iny ? 0.5 * a.g.inv[1] : a.g.inv[1];
+      gxa = (float)((uc[1] - left) * dxa), gxb = (float)((right - uc[0]) * dxb);
+      gya = (float)((uq0 - um[0]) * dy), gyb = (float)((uq1 - um[1]) * dy);
+    }
     const float ira = rsqrt_fast(fmaf(gxa, gxa, fmaf(gya, gya, e2)));
     const float irb = rsqrt_fast(fmaf(gxb, gxb, fmaf(gyb, gyb, e2)));
     const float nxa = gxa * ira, nya = gya * ira;

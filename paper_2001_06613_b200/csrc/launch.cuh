@@ -190,7 +190,7 @@ inline cudaError_t ngf_sfeat_d2(const Launch& L, const Args& a, const NgfBufs& B
   const auto al8 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 7) == 0; };
   const double e2 = a.eps * a.eps;
   const long long smax = 1LL << 30;  // 32-bit index arithmetic inside a frame's rows
-  if (a.g.pow2 && n0 >= 2 && n0 % 2 == 0 && a.g.n[1] >= 2 && e2 > 1e-30 && e2 < 1e30 && al8(B.Nf) && al8(B.Rho) &&
+  if (n0 >= 2 && n0 % 2 == 0 && a.g.n[1] >= 2 && e2 > 1e-30 && e2 < 1e30 && al8(B.Nf) && al8(B.Rho) &&
       al8(B.G) && ((B.zlo | B.zstride | B.vlo | B.vstride) & 1) == 0 && a.y_stride < smax && B.zstride < smax &&
       B.vstride < smax && a.g.N < smax && !(getenv("SEQREG_B200_SFEAT") && getenv("SEQREG_B200_SFEAT")[0] == '0')) {
     // one warp per (chunk of 62 columns, segment of rows, frame): segments as long as >= 4 waves of 32 warps
@@ -202,8 +202,12 @@ inline cudaError_t ngf_sfeat_d2(const Launch& L, const Args& a, const NgfBufs& B
     const int nseg = (rz1 - rz0 + segf - 1) / segf;
     if (nseg <= 65535 && a.K <= 65535) {
       const dim3 wgrid((unsigned)nchunk, (unsigned)nseg, (unsigned)a.K);
-      k_ngf_sfeat2f<32><<<wgrid, 32, 0, L.stream>>>(a, segf, rz0, rz1, rs0, rs1, B.Nf, B.Rho, B.zlo, B.zstride, B.G,
-                                                    B.vlo, B.vstride);
+      if (a.g.pow2)
+        k_ngf_sfeat2f<32, true><<<wgrid, 32, 0, L.stream>>>(a, segf, rz0, rz1, rs0, rs1, B.Nf, B.Rho, B.zlo, B.zstride,
+                                                            B.G, B.vlo, B.vstride);
+      else
+        k_ngf_sfeat2f<32, false><<<wgrid, 32, 0, L.stream>>>(a, segf, rz0, rz1, rs0, rs1, B.Nf, B.Rho, B.zlo, B.zstride,
+                                                             B.G, B.vlo, B.vstride);
       return cudaGetLastError();
     }
     return cudaGetLastError();

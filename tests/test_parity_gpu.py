@@ -489,9 +489,10 @@ def test_context_orders_calls_across_streams():
         assert torch.equal(gi, g0)
 
 
+@pytest.mark.parametrize("sp", [(0.5, 0.25), (0.3, 0.7)])  # power-of-two and general spacings (POW2 template)
 @pytest.mark.parametrize("dims,K", [((62, 5), 3), ((64, 2), 4), ((126, 9), 5), ((130, 40), 40), ((2, 7), 3),
                                     ((1024, 3), 2), ((190, 70), 70)])
-def test_ngf_fast_sampler_matches_generic(dims, K):
+def test_ngf_fast_sampler_matches_generic(dims, K, sp):
     """k_ngf_sfeat2f (one warp per 62-column chunk and row segment, shuffles, rsqrt.approx) against the generic
     k_ngf_sfeat2 (SEQREG_B200_SFEAT=0, read at launch) on ragged shapes: a single chunk, a chunk of 2 columns,
     2- and 3-row images (every look-ahead row missing), several segments, K in each Gram bucket.  Same D to
@@ -500,7 +501,7 @@ def test_ngf_fast_sampler_matches_generic(dims, K):
     import os
 
     rng = np.random.default_rng(11)
-    sp, org = (0.5, 0.25), (-3.0, 1.0)
+    org = (-3.0, 1.0)
     from scipy.ndimage import gaussian_filter
 
     frames = np.stack([gaussian_filter(rng.standard_normal(dims), 1.2, mode="reflect").ravel(order="F") + 2.0
