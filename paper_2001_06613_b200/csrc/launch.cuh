@@ -176,43 +176,42 @@ struct NgfBufs {
   long long vlo, vhi, vstride, zlo, zhi, zstride;
 };
 
-// 2-D fused sampling + NGF feature (k_ngf_sfeat2) over the NgfBufs ranges; NotSupported when a row does
-// not fit one CTA (n0 > 1024) or the ranges are not whole rows
+// 2-D fused sampling + NGF feature over the NgfBufs ranges (k_ngf_sfeat2f, else the generic k_ngf_sfeat2);
+// NotSupported when the ranges are not whole rows (or, generic kernel only, a row does not fit one CTA)
 inline cudaError_t ngf_sfeat_d2(const Launch& L, const Args& a, const NgfBufs& B) {
   const int n0 = a.g.n[0];
-  if (a.g.nd != 2 || n0 > 1024 || (B.zlo % n0) || (B.zhi % n0) || (a.pix_lo % n0) || (a.pix_hi % n0))  // 512 x 2
-    return cudaErrorNotSupported;
+  if (a.g.nd != 2 || (B.zlo % n0) || (B.zhi % n0) || (a.pix_lo % n0) || (a.pix_hi % n0)) return cudaErrorNotSupported;
   const int rz0 = (int)(B.zlo / n0), rz1 = (int)(B.zhi / n0);
   const int rs0 = (int)(a.pix_lo / n0), rs1 = (int)(a.pix_hi / n0);
-  int seg = 32;
-  while (seg > 8 && (long long)((rz1 - rz0 + seg - 1) / seg) * a.K < 8LL * L.sms) seg /= 2;
-  const dim3 grid((unsigned)((rz1 - rz0 + seg - 1) / seg), (unsigned)a.K);
   const auto al8 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 7) == 0; };
   const double e2 = a.eps * a.eps;
   const long long smax = 1LL << 30;  // 32-bit index arithmetic inside a frame's rows
-  if (n0 >= 2 && n0 % 2 == 0 && a.g.n[1] >= 2 && e2 > 1e-30 && e2 < 1e30 && al8(B.Nf) && al8(B.Rho) &&
-      al8(B.G) && ((B.zlo | B.zstride | B.vlo | B.vstride) & 1) == 0 && a.y_stride < smax && B.zstride < smax &&
-      B.vstride < smax && a.g.N < smax && !(getenv("SEQREG_B200_SFEAT") && getenv("SEQREG_B200_SFEAT")[0] == '0')) {
-    // one warp per (chunk of 62 columns, segment of rows, frame): segments as long as >= 4 waves of 32 warps
-    // per SM allow (every segment re-samples 2 halo rows and pays an unpipelined prologue)
-    const int nchunk = (n0 + 61) / 62;
-    int segf = 32;
-    if (const char* sv = getenv("SEQREG_B200_SFSEG")) segf = atoi(sv) > 0 ? atoi(sv) : segf;
-    while (segf > 8 && (long long)((rz1 - rz0 + segf - 1) / segf) * nchunk * a.K < 4LL * 32 * L.sms) segf /= 2;
-    const int nseg = (rz1 - rz0 + segf - 1) / segf;
-    if (nseg <= 65535 && a.K <= 65535) {
-      const dim3 wgrid((unsigned)nchunk, (unsigned)nseg, (unsigned)a.K);
-      if (a.g.pow2)
-        k_ngf_sfeat2f<32, true><<<wgrid, 32, 0, L.stream>>>(a, segf, rz0, rz1, rs0, rs1, B.Nf, B.Rho, B.zlo, B.zstride,
-                                                            B.G, B.vlo, B.vstride);
-      else
-        k_ngf_sfeat2f<32, false><<<wgrid, 32, 0, L.stream>>>(a, segf, rz0, rz1, rs0, rs1, B.Nf, B.Rho, B.zlo, B.zstride,
-                                                             B.G, B.vlo, B.vstride);
-      return cudaGetLastError();
-    }
+  // k_ngf_sfeat2f: one warp per (chunk of 62 columns, segment of rows, frame), any row length; segments as long
+  // as >= 4 waves of 32 warps per SM allow (every segment re-samples 2 halo rows and pays an unpipelined prologue)
+  const int nchunk = (n0 + 61) / 62;
+  int segf = 32;
+  if (const char* sv = getenv("SEQREG_B200_SFSEG")) segf = atoi(sv) > 0 ? atoi(sv) : segf;
+  while (segf > 8 && (long long)((rz1 - rz0 + segf - 1) / segf) * nchunk * a.K < 4LL * 32 * L.sms) segf /= 2;
+  const long long nseg = (rz1 - rz0 + segf - 1) / segf;
+  if (n0 >= 2 && n0 % 2 == 0 && a.g.n[1] >= 2 && e2 > 1e-30 && e2 < 1e30 && al8(B.Nf) && al8(B.Rho) && al8(B.G) &&
+      ((B.zlo | B.zstride | B.vlo | B.vstride) & 1) == 0 && a.y_stride < smax && B.zstride < smax &&
+      B.vstride < smax && a.g.N < smax && nseg <= 65535 && a.K <= 65535 &&
+      !(getenv("SEQREG_B200_SFEAT") && getenv("SEQREG_B200_SFEAT")[0] == '0')) {
+    const dim3 wgrid((unsigned)nchunk, (unsigned)nseg, (unsigned)a.K);
+    if (a.g.pow2)
+      k_ngf_sfeat2f<32, true><<<wgrid, 32, 0, L.stream>>>(a, segf, rz0, rz1, rs0, rs1, B.Nf, B.Rho, B.zlo, B.zstride,
+                                                          B.G, B.vlo, B.vstride);
+    else
+      k_ngf_sfeat2f<32, false><<<wgrid, 32, 0, L.stream>>>(a, segf, rz0, rz1, rs0, rs1, B.Nf, B.Rho, B.zlo, B.zstride,
+                                                           B.G, B.vlo, B.vstride);
     return cudaGetLastError();
   }
-  constexpr int PX = 2;  // columns per thread: 512 threads for a 1024-pixel row
+  // generic k_ngf_sfeat2: a whole row per CTA of 2 columns per thread (n0 <= 1024)
+  if (n0 > 1024) return cudaErrorNotSupported;
+  int seg = 32;
+  while (seg > 8 && (long long)((rz1 - rz0 + seg - 1) / seg) * a.K < 8LL * L.sms) seg /= 2;
+  const dim3 grid((unsigned)((rz1 - rz0 + seg - 1) / seg), (unsigned)a.K);
+  constexpr int PX = 2;
   const int nt = ((n0 + PX - 1) / PX + 31) / 32 * 32;
   if (a.g.pow2)
     k_ngf_sfeat2<true, PX><<<grid, nt, 0, L.stream>>>(a, seg, rz0, rz1, rs0, rs1, B.Nf, B.Rho, B.zlo, B.zstride,

@@ -491,7 +491,7 @@ def test_context_orders_calls_across_streams():
 
 @pytest.mark.parametrize("sp", [(0.5, 0.25), (0.3, 0.7)])  # power-of-two and general spacings (POW2 template)
 @pytest.mark.parametrize("dims,K", [((62, 5), 3), ((64, 2), 4), ((126, 9), 5), ((130, 40), 40), ((2, 7), 3),
-                                    ((1024, 3), 2), ((190, 70), 70)])
+                                    ((1024, 3), 2), ((190, 70), 70), ((2048, 6), 2)])
 def test_ngf_fast_sampler_matches_generic(dims, K, sp):
     """k_ngf_sfeat2f (one warp per 62-column chunk and row segment, shuffles, rsqrt.approx) against the generic
     k_ngf_sfeat2 (SEQREG_B200_SFEAT=0, read at launch) on ragged shapes: a single chunk, a chunk of 2 columns,
@@ -538,4 +538,7 @@ def test_ngf_fast_sampler_matches_generic(dims, K, sp):
     yq = y.astype(np.float32).astype(np.float64)
     _, Dref, gref = orc.evaluate_field(list(q), dims, sp, org, yq, w, h, "ngf", 0.3)
     assert Df == pytest.approx(Dref, rel=1e-4)
-    assert _relmax(gf, gref) < 1e-4
+    # 2048 cells of a general spacing: the fp32 coordinate (p - o) / s itself resolves 2048 * 6e-8 = 1.2e-4 cells,
+    # so the fractions (and the gradient of the bilinear interpolant) of both samplers carry that
+    tol = 1e-4 if dims[0] <= 1024 else 5e-4
+    assert _relmax(gf, gref) < tol
