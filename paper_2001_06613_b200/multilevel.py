@@ -173,6 +173,25 @@ def _solve(lvl: DeviceFrames, subset, init: torch.Tensor, w, cfg: FieldRunConfig
         grad = g.reshape(-1).to(torch.float64)
         return ObjectiveEval(float(value.item()), grad * c if c != 1.0 else grad)
 
+    def evaluate_into(x: torch.Tensor, g_out: torch.Tensor) -> float:
+        """The same objective without n-vector temporaries (the fields of C5's finest level are 1 GB in fp64):
+        y = c x in one pass (the fp64 product rounded once into y's dtype, as above), the gradient scaled by c
+        straight into the solver's fp64 buffer (an fp64 gradient exactly as above; an fp32 one is scaled in
+        fp32 before the widening)."""
+        if c != 1.0:
+            torch.mul(x.view(shape), c, out=y)
+        else:
+            y.copy_(x.view(shape))
+        stats, _ = obj.evaluate(y, g)
+        value = stats[0] + obj.s_reg[0] if cfg.alpha > 0 else stats[0]
+        if c != 1.0:
+            torch.mul(g.reshape(-1), c, out=g_out)
+        else:
+            g_out.copy_(g.reshape(-1))
+        return float(value.item())
+
+    objective.evaluate_into = evaluate_into
+
     x0 = init.to(torch.float64).reshape(-1)
     x0 = (x0 / c if c != 1.0 else x0).contiguous()
     res = lbfgs_minimize(objective, x0, cfg.optim, engine=lvl.engine)

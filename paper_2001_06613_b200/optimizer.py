@@ -120,6 +120,13 @@ def lbfgs_minimize(objective, x0, opts: OptimOptions | None = None, trace=None, 
     def _objective(user, x_ptr, f_out, g_ptr):
         try:
             xv = _device_view(x_ptr, n, dev)
+            if device_mode and hasattr(objective, "evaluate_into"):
+                # device objectives may write the fp64 gradient straight into the solver's buffer (no
+                # intermediate copies of n-vectors): evaluate_into(x, g_out) -> value
+                value = objective.evaluate_into(xv, _device_view(g_ptr, n, dev))
+                torch.cuda.synchronize(dev)
+                f_out[0] = float(value)
+                return 0
             arg = xv if device_mode else xv.cpu().numpy()
             e = objective(arg)
             g = e.gradient
