@@ -787,7 +787,7 @@ static int grad_impl_core(sr_ctx* c, const sr_problem* p, const double* stats, v
     }
     CK(d == 2 ? ngf_pass2_d2(L, a, c->vtag.ngf) : ngf_pass2_d3(L, a, c->vtag.ngf));
     if (fuse) {
-      k_reduce<<<1, 256, 0, c->stream>>>(c->curv_part, nb, 1, 1, 1, 1, c->curv_s);
+      k_sum1<<<1, 1024, 0, c->stream>>>(c->curv_part, nb, c->curv_s);
       CK(cudaGetLastError());
       *curv_done = true;
     }
@@ -1033,7 +1033,7 @@ static int curvature_impl(sr_ctx* c, const sr_problem* p, double alpha, double h
   a.o_stride = g_stride;
   int nb = 0;
   CK(SR_SWITCH(p->dtype, d, curvature, launch_of(c), a, alpha, h, c->aux, c->aux_cap, &nb));
-  k_reduce<<<1, 256, 0, c->stream>>>(c->aux, nb, 1, 1, 1, 1, s_out);
+  k_sum1<<<1, 1024, 0, c->stream>>>(c->aux, nb, s_out);
   CK(cudaGetLastError());
   return SR_OK;
 }

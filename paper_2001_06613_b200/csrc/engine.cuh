@@ -4,7 +4,7 @@
 //                          raw Gram G = sum_rows v v^T plus per-frame sum / max / min.
 //                          Replaces correlation_state (similarity.py:128-164) with
 //                          sample (grid.py:236-243) and feature (similarity.py:73-87) fused.
-// Reduce  (k_reduce)     : fixed-order cross-CTA sum (deterministic, no float atomics,
+// Reduce  (k_reduce_finalize, k_sum1): fixed-order cross-CTA sums (deterministic, no float atomics,
 //                          SPEC.md:318 determinism).
 // Finalize(k_finalize)   : centre/normalise -> C, degenerate flags, D (similarity.py:167-177)
 //                          and the gradient coefficients M', beta'.
@@ -44,7 +44,7 @@ struct Args {
   int ymap_ok;          // a y tensor map was encoded for the warp-specialized kernels
   double curv_alpha;    // > 0: pass 2 adds the curvature gradient alpha h L L (y - x) (sr_evaluate_reg)
   double curv_h;
-  double* curv_part;    // per-CTA partial sums of S (reduced by k_reduce)
+  double* curv_part;    // per-CTA partial sums of S (reduced by k_sum1)
 };
 
 // --------------------------------------------------------- stats buffer layout
@@ -493,30 +493,30 @@ __global__ void __launch_bounds__(G1<T, KP, FEAT>::NT) k_pass1(const Args a) {
   else pass1_body<T, D, FEAT, PARAM, KP, false>(a);
 }
 
-// Fixed-order reduction of per-CTA partials (used for small partial sets, e.g. S(y)):
-// block handles 32 consecutive elements, warp w sums CTAs w, w+8, ...; warp 0 combines
-// the 8 warp sums in order.  Elements in [n_sum, n_max_end) are max-reduced.
-static __global__ void __launch_bounds__(256) k_reduce(const double* __restrict__ part, int nblk,
-                                                       int stride, int n_sum, int n_max_end, int n_total,
-                                                       double* __restrict__ red) {
-  __shared__ double buf[8][33];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int e = blockIdx.x * 32 + lane;
-  const bool is_max = e >= n_sum && e < n_max_end;
-  double acc = is_max ? -INFINITY : 0.0;
-  if (e < n_total) {
-    for (int b = warp; b < nblk; b += 8) {
-      const double v = part[(size_t)b * stride + e];
-      acc = is_max ? fmax(acc, v) : acc + v;
+// Fixed-order sum of n partials into one scalar (S(y): one partial per CTA of the curvature kernels, 65,536 at
+// C5's finest level, where the generic partial reduction's single active lane per warp took 2 ms): thread t sums partials
+// t, t + 1024, ... in batches of 8 independent loads, then a fixed tree over the 1024 thread sums.
+static __global__ void __launch_bounds__(1024) k_sum1(const double* __restrict__ part, int n, double* __restrict__ out) {
+  __shared__ double buf[1024];
+  const int t = threadIdx.x;
+  double acc = 0.0;
+  for (int b0 = t; b0 < n; b0 += 8 * 1024) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int b = b0 + 1024 * u;
+      v[u] = b < n ? __ldcg(part + b) : 0.0;
     }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += v[u];
   }
-  buf[warp][lane] = acc;
+  buf[t] = acc;
   __syncthreads();
-  if (warp == 0 && e < n_total) {
-    double s = buf[0][lane];
-    for (int w = 1; w < 8; ++w) s = is_max ? fmax(s, buf[w][lane]) : s + buf[w][lane];
-    red[e] = s;
+  for (int o = 512; o > 0; o >>= 1) {
+    if (t < o) buf[t] += buf[t + o];
+    __syncthreads();
   }
+  if (t == 0) *out = buf[0];
 }
 
 // ==================================================================== finalize

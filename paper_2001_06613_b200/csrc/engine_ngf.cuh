@@ -145,6 +145,62 @@ __global__ void __launch_bounds__(256) k_ngf_feat4(const Args a, const float* __
 // CURV (sr_evaluate_reg): the curvature gradient alpha h L L (y - x) of the same pixels is added to the
 // output in the same launch (same arithmetic and the same float addition as k_curvature after this kernel),
 // and the CTA's share of S goes to a.curv_part[blockIdx.y * gridDim.x + blockIdx.x].
+// alpha h (L L u) of 4 consecutive pixels of one row (2-D, u = y - x of one component) and their share of S,
+// the arithmetic of curv_grad_at / lap_u (Neumann Laplacian: a missing neighbour is the value itself, i.e. every
+// index clamped into the grid, first for the position of a Laplacian, then for its neighbours) with the u patch
+// loaded once: rows j - 2 .. j + 2, 28 values and 14 Laplacians for the 4 pixels instead of 100 and 20 (the
+// per-pixel form costs ~1000 fp64 instructions per voxel-frame and made sr_evaluate_reg 5x a plain evaluation).
+template <typename T>
+__device__ __forceinline__ void curv4_d2(const Args& a, const T* __restrict__ yc, int comp, long long p0, int c0,
+                                         int c1, int nvalid, double alpha, double h, float (&cv)[4], double& sval) {
+  const int n0 = a.g.n[0], n1 = a.g.n[1];
+  const long long st1 = a.g.st[1];
+  const double i0 = a.g.inv[0], i1 = a.g.inv[1];
+  const T* yb = yc + (p0 - a.y_off);
+  auto U = [&](int i, int j) -> double {  // u at the clamped (i, j)
+    const int ic = min(max(i, 0), n0 - 1), jc = min(max(j, 0), n1 - 1);
+    const double ctr = comp == 0 ? center(a.g, 0, ic) : center(a.g, 1, jc);
+    return (double)ldg(yb + (ic - c0) + (long long)(jc - c1) * st1) - ctr;
+  };
+  double r0[4], r1[6], r2[8], r3[6], r4[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) r0[e] = U(c0 + e, c1 - 2), r4[e] = U(c0 + e, c1 + 2);
+#pragma unroll
+  for (int e = 0; e < 6; ++e) r1[e] = U(c0 - 1 + e, c1 - 1), r3[e] = U(c0 - 1 + e, c1 + 1);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) r2[e] = U(c0 - 2 + e, c1);
+  double lc[6], lu[4], ld[4];
+#pragma unroll
+  for (int e = 0; e < 6; ++e) {  // Laplacian at (c0 - 1 + e, c1)
+    double o = 0.0;
+    o += (r2[e + 2] - 2.0 * r2[e + 1] + r2[e]) * i0 * i0;
+    o += (r3[e] - 2.0 * r2[e + 1] + r1[e]) * i1 * i1;
+    lc[e] = o;
+  }
+  if (c0 == 0) lc[0] = lc[1];            // position -1 := position 0
+  if (c0 + 4 >= n0) lc[5] = lc[4];       // position n0 := position n0 - 1
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {  // Laplacians at (c0 + t, c1 - 1) and (c0 + t, c1 + 1)
+    double o = 0.0;
+    o += (r1[t + 2] - 2.0 * r1[t + 1] + r1[t]) * i0 * i0;
+    o += (r2[t + 2] - 2.0 * r1[t + 1] + r0[t]) * i1 * i1;
+    lu[t] = c1 > 0 ? o : lc[t + 1];
+    double q = 0.0;
+    q += (r3[t + 2] - 2.0 * r3[t + 1] + r3[t]) * i0 * i0;
+    q += (r4[t] - 2.0 * r3[t + 1] + r2[t + 2]) * i1 * i1;
+    ld[t] = c1 < n1 - 1 ? q : lc[t + 1];
+  }
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const double l0 = lc[t + 1];
+    double ll = 0.0;
+    ll += (lc[t + 2] - 2.0 * l0 + lc[t]) * i0 * i0;
+    ll += (ld[t] - 2.0 * l0 + lu[t]) * i1 * i1;
+    cv[t] = (float)(alpha * h * ll);
+    if (t < nvalid) sval += 0.5 * alpha * h * l0 * l0;
+  }
+}
+
 // (D_h^T z) terms of one axis at index i of n: rows i - 1, i + 1 (interior) and the one-sided edge rows
 // (dgrad_adjoint); zm, z0, zp = z at i - 1, i, i + 1 (any finite value where the row does not exist)
 __device__ __forceinline__ float adj_terms(int i, int n, float zm, float z0, float zp, float h2, float inv) {
@@ -284,6 +340,9 @@ __global__ void __launch_bounds__(256) k_ngf_adj4(const Args a, const float* __r
       const float* yc = reinterpret_cast<const float*>(a.y) + (long long)(k * D + cc) * a.y_stride;
       int cq[3];
       coords_flat(a.g, p0, cq);
+      if (D == 2 && (a.g.n[0] & 3) == 0 && (cq[0] & 3) == 0 && q0 + 4 <= npix) {
+        curv4_d2<float>(a, yc, cc, p0, cq[0], cq[1], 4, a.curv_alpha, a.curv_h, cv, sval);
+      } else
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         if (q0 + t < npix) cv[t] = (float)curv_grad_at<float, D>(a, yc, cc, p0 + t, cq, a.curv_alpha, a.curv_h, sval);
