@@ -130,6 +130,9 @@ __global__ void k_nonfinite(const double* __restrict__ a, long long n, int* __re
 
 struct Workspace {
   long long n = 0;
+  long long cap = 0;  // entries every n-vector is allocated for (grow-only: a multilevel run solves problems of
+                      // 16 different sizes, and cudaFree / cudaMalloc of its 14 vectors, 1 GB each at C5's finest
+                      // level, cost more than the solves)
   int m = 0;
   double *g = nullptr, *p = nullptr, *xn = nullptr, *gn = nullptr, *partial = nullptr, *scal = nullptr;
   std::vector<double*> S, Y;
@@ -179,9 +182,13 @@ static cudaError_t reduce(const Ctx& c, Workspace& w, long long n, int nr, const
   } while (0)
 
 static int ensure(Workspace& w, long long n, int m, char* err, size_t errlen) {
-  if (w.n == n && w.m == m && w.g) return SR_OK;
+  if (w.cap >= n && w.m == m && w.g) {
+    w.n = n;
+    return SR_OK;
+  }
   w.release();
   w.n = n;
+  w.cap = n;
   w.m = m;
   const size_t b = (size_t)n * sizeof(double);
   LK(cudaMalloc(&w.g, b));
