@@ -1,3 +1,5 @@
+"""Diagnostic (GPU box): the pieces of one regularised objective call of the C5 finest level (y = c x, sr_evaluate_reg,
+value readback, gradient scaling), two solver vector operations, and the per-kernel device times of the evaluation."""
 import sys, time, numpy as np, torch
 sys.path.insert(0, '/root/repo')
 import paper_2001_06613_b200 as srb
